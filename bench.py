@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 block ILU(k) hot path -- one JSON line on rank 0.
+
+Step = one preconditioner apply (L y = b, z = D^-1 y, U' x = z) of the
+128^3-cell, 3x3-block, ILU(0) synthetic reservoir system (BASELINE.json
+configs[2]), with the right-hand side already resident in HBM.  Metric:
+algorithmic apply bandwidth in GB/s, B_apply / t:
+
+    B_apply = 8 b^2 (nL + nU + n) + 4 (nL + nU) + 8 (n + 1) + 32 b n
+
+Also reported: e2e (the same metric through the public API from pinned host
+memory, copies inside the timed region), solves/s, the ILU(2) sweep of the
+same grid, BiCGSTAB time-to-1e-6 (ILU(0)), setup time, the roofline of the
+sweep kernel and a CPU baseline (the oracle port of the reference apply).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): every rank solves its own independent 128^3 system
+(weak scaling, no data-path collective); `value` = total bytes / max-rank time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nx", type=int, default=128)
+    ap.add_argument("--bs", type=int, default=3)
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip ILU(2), BiCGSTAB and CPU baseline legs")
+    ap.add_argument("--cpu-nx", type=int, default=64, help="grid edge of the CPU-baseline sample")
+    return ap.parse_args()
+
+
+def apply_bytes(info):
+    b, n, nL, nU = info["bs"], info["n"], info["nL"], info["nU"]
+    return 8 * b * b * (nL + nU + n) + 4 * (nL + nU) + 8 * (n + 1) + 32 * b * n
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU apply (oracle port) on this host's cores."""
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    from oracle import cbaseline
+    res = cbaseline.measure(args.nx, args.bs, args.k, steps=args.steps, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": "ilu_apply_GBps", "value": res["GBps"], "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["ms_per_apply"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8d generator, seed 0)",
+        "config": {"workload": f"apply {args.nx}^3 b{args.bs} ILU({args.k})", "grid": args.nx, "bs": args.bs,
+                   "k": args.k},
+        "cpu_baseline": {"value": res["GBps"], "unit": "GB/s", "cores": res["cores"], "kind": res["kind"],
+                         "sample": res["sample"]},
+        "e2e": {"value": res["GBps"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1703_01325_b200 as b2
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- build the system and the preconditioner -------------------------
+    t0 = time.perf_counter()
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(args.nx, args.nx, args.nx, args.bs, seed=rank)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    t_gen = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f = b2.build_preconditioner(a, args.k)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    info = f.info
+    B = apply_bytes(info)
+    assert B == info["apply_bytes"]
+    length = n * bs
+    rhs = torch.from_numpy(np.random.default_rng(1).standard_normal(length)).cuda()
+    out = torch.empty_like(rhs)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- device-resident timing ------------------------------------------
+    for _ in range(args.warmup):
+        b2.apply_preconditioner(f, rhs, out=out)
+    f.status()
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            b2.apply_preconditioner(f, rhs, out=out)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    f.status()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t_kernel_ms = float(np.mean(per))
+    if dist is not None:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B / (ms_per_step * 1e-3) / 1e9
+
+    # ---------------- e2e through the public API, pinned host buffers -----------------
+    host_in = torch.from_numpy(np.random.default_rng(1).standard_normal(length)).pin_memory()
+    host_out = torch.empty(length, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, args.steps // 2)
+
+    def e2e_step():
+        dev_in = host_in.to("cuda", non_blocking=True)
+        x = b2.apply_preconditioner(f, dev_in)
+        host_out.copy_(x, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist is not None:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = world * B / (e2e_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = B / (t_kernel_ms * 1e-3) / 1e9
+
+    extras = {}
+    if not args.no_extras:
+        # BiCGSTAB time-to-1e-6 with this preconditioner (b = A 1, x0 = 0)
+        bvec = torch.from_numpy(b2.synthetic.ones_rhs(n, bs, rp, ci, vals)).cuda()
+        b2.bicgstab(a, bvec, M=f, cfg=b2.SolverConfig(rel_tol=1e-6))     # warm (operator upload)
+        barrier()
+        t0 = time.perf_counter()
+        _, st = b2.bicgstab(a, bvec, M=f, cfg=b2.SolverConfig(rel_tol=1e-6))
+        torch.cuda.synchronize()
+        extras["bicgstab"] = {"seconds": time.perf_counter() - t0, "iterations": st.iterations,
+                              "converged": st.converged, "true_rel_residual": st.final_relative_residual,
+                              "precond": f"ILU({args.k})"}
+        # ILU(2) sweep of the same grid (configs[2] "ILU(0) and ILU(2)")
+        if args.k != 2:
+            t0 = time.perf_counter()
+            f2 = b2.build_preconditioner(a, 2)
+            torch.cuda.synchronize()
+            s2 = time.perf_counter() - t0
+            B2 = apply_bytes(f2.info)
+            for _ in range(3):
+                b2.apply_preconditioner(f2, rhs, out=out)
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(stream)
+            for _ in range(10):
+                b2.apply_preconditioner(f2, rhs, out=out)
+            q1.record(stream)
+            torch.cuda.synchronize()
+            f2.status()
+            ms2 = q0.elapsed_time(q1) / 10
+            extras["ilu2_apply"] = {"GBps": B2 / (ms2 * 1e-3) / 1e9, "ms": ms2, "bytes": B2,
+                                    "frac_of_measured_hbm": B2 / (ms2 * 1e-3) / 1e9 / peak, "setup_s": s2,
+                                    "levels": [f2.info["levels_L"], f2.info["levels_U"]]}
+            del f2
+
+    cpu = None
+    if rank == 0 and not args.no_extras:
+        try:
+            from oracle import cbaseline
+            r = cbaseline.measure(args.cpu_nx, args.bs, args.k, steps=3, warmup=1)
+            cpu = {"value": r["GBps"], "unit": "GB/s", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
+        except Exception as exc:   # reported, never fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "ilu_apply_GBps", "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8d reservoir generator, seed = rank)",
+            "config": {"workload": f"ILU({args.k}) apply, {args.nx}^3 cells, {bs}x{bs} BSR (BASELINE configs[2])",
+                       "grid": args.nx, "bs": bs, "k": args.k, "n_block_rows": n, "nL": info["nL"],
+                       "nU": info["nU"], "levels": [info["levels_L"], info["levels_U"]],
+                       "bytes_per_apply": B, "l2": "working set 1.3+ GB >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"replicas x{world} (independent systems, no collective)"},
+            "solves_per_s": world / (ms_per_step * 1e-3),
+            "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * length,
+                    "d2h_bytes_per_step": 8 * length, "ms_per_step": e2e_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "sweep_kernel<3> (L and U' sweeps, one persistent launch)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps,
+            "setup_s": t_setup, "gen_s": t_gen,
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

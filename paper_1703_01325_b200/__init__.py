@@ -1,0 +1,40 @@
+"""B200-native block ILU(k) preconditioner (arXiv 1703.01325) -- drop-in for the
+reference package ``blockiluk``'s factor / apply / Krylov entry points.
+
+Host code here is thin: index containers, argument checks and exception
+mapping.  Every numeric step of the path runs as hand-written sm_100a CUDA in
+``_lib/libbiluk.so`` (C ABI: ``include/biluk.h``); torch tensors are used as
+device buffers only.  There is no CPU fallback.
+"""
+
+from .errors import FactorizationError, SingularBlockError, StructuralError
+from .factor import BlockIlukFactors, build_preconditioner, symbolic_phase
+from .krylov import SolverConfig, SolveStats, bicgstab, gmres
+from .sparse import (BcsrMatrix, CsrMatrix, PatternMatrix, bcsr_from_csr, csr_expand, csr_from_triplets,
+                     extract_point_pattern)
+from .trisolve import (LevelSchedule, TriangularOperand, apply_preconditioner, build_level_schedule,
+                       strict_triangle)
+from .device import DeviceOperator
+from .synthetic import reservoir_block_grid
+
+__version__ = "0.1.0"
+
+
+def spmv(a, x, workers=1):
+    """y = a @ x on the GPU (reference sparse.py:278-301); numpy in -> numpy out."""
+    import numpy as np
+    from .device import operator_for, torch
+    t = torch()
+    y = operator_for(a).matvec(x)
+    if isinstance(x, t.Tensor) and x.is_cuda:
+        return y
+    return y.cpu().numpy()
+
+
+__all__ = [
+    "BcsrMatrix", "BlockIlukFactors", "CsrMatrix", "DeviceOperator", "FactorizationError", "LevelSchedule",
+    "PatternMatrix", "SingularBlockError", "SolveStats", "SolverConfig", "StructuralError", "TriangularOperand",
+    "apply_preconditioner", "bcsr_from_csr", "bicgstab", "build_level_schedule", "build_preconditioner",
+    "csr_expand", "csr_from_triplets", "extract_point_pattern", "gmres", "reservoir_block_grid", "spmv",
+    "strict_triangle", "symbolic_phase", "__version__",
+]

@@ -1,0 +1,353 @@
+// extern "C" surface of libbiluk (declared in include/biluk.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "biluk_internal.h"
+#include "kernels.cuh"
+
+struct biluk_pattern {
+    int64_t n = 0;
+    std::vector<int32_t> rp, ci;
+};
+
+namespace biluk {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+static int cuda_fail(cudaError_t e, const char *what) {
+    return fail(BILUK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_TRY(expr, what)                          \
+    do {                                              \
+        cudaError_t _e = (expr);                      \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+static DevStatus *dev_status(Plan &p) { return reinterpret_cast<DevStatus *>(p.ws + p.off.status); }
+
+int64_t apply_bytes(const Plan &p) {
+    // 8b^2(nL+nU+n) + 4(nL+nU) + 8(n+1) + 32bn
+    const int64_t b = p.bs;
+    return 8 * b * b * (p.nL + p.nU + p.n) + 4 * (p.nL + p.nU) + 8 * (p.n + 1) + 32 * b * p.n;
+}
+int64_t spmv_bytes(const Plan &p) {
+    const int64_t b = p.bs;
+    return 8 * b * b * p.nnzA + 4 * p.nnzA + 4 * (p.n + 1) + 16 * b * p.n;
+}
+
+}  // namespace biluk
+
+using namespace biluk;
+
+extern "C" {
+
+const char *biluk_last_error(void) { return g_err.c_str(); }
+
+int biluk_set_device(int32_t device) {
+    CUDA_TRY(cudaSetDevice(device), "set device");
+    return BILUK_OK;
+}
+const char *biluk_version(void) { return "biluk 0.1.0 (sm_100a)"; }
+
+int biluk_symbolic(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t k, biluk_pattern_t **out,
+                   int64_t *err_row) {
+    if (!out) return fail(BILUK_EARG, "null output");
+    *out = nullptr;
+    if (k < 0) return fail(BILUK_EARG, "fill level k must be nonnegative");
+    if (n < 0 || n >= INT32_MAX || (n > 0 && row_ptr[n] >= INT32_MAX))
+        return fail(BILUK_EUNSUPPORTED, "pattern exceeds 2^31 entries");
+    std::vector<int32_t> rp(n + 1), ci(n ? row_ptr[n] : 0);
+    for (int64_t i = 0; i <= n; ++i) rp[i] = int32_t(row_ptr[i]);
+    for (size_t t = 0; t < ci.size(); ++t) ci[t] = int32_t(col_idx[t]);
+    auto *pat = new (std::nothrow) biluk_pattern;
+    if (!pat) return fail(BILUK_ENOMEM, "out of host memory");
+    pat->n = n;
+    int rc = symbolic_phase(n, rp.data(), ci.data(), k, pat->rp, pat->ci, err_row);
+    if (rc != BILUK_OK) {
+        delete pat;
+        return rc;
+    }
+    *out = pat;
+    return BILUK_OK;
+}
+
+int64_t biluk_pattern_nnz(const biluk_pattern_t *p) { return p ? int64_t(p->ci.size()) : -1; }
+
+int biluk_pattern_copy(const biluk_pattern_t *p, int64_t *row_ptr, int64_t *col_idx) {
+    if (!p) return fail(BILUK_EARG, "null pattern");
+    for (int64_t i = 0; i <= p->n; ++i) row_ptr[i] = p->rp[i];
+    for (size_t t = 0; t < p->ci.size(); ++t) col_idx[t] = p->ci[t];
+    return BILUK_OK;
+}
+
+void biluk_pattern_free(biluk_pattern_t *p) { delete p; }
+
+int biluk_level_schedule(int64_t m, const int64_t *row_ptr, const int64_t *col_idx, int32_t upper,
+                         int64_t *level_of_row, int64_t *num_levels) {
+    if (m < 0) return fail(BILUK_EARG, "negative dimension");
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t t = row_ptr[i]; t < row_ptr[i + 1]; ++t) {
+            const int64_t j = col_idx[t];
+            if (j < 0 || j >= m || (upper ? j <= i : j >= i))
+                return fail(BILUK_ESTRUCT, std::string("entry on or across the diagonal in a ") +
+                                               (upper ? "upper" : "lower") + " operand");
+        }
+    level_schedule(m, row_ptr, col_idx, upper != 0, level_of_row, num_levels);
+    return BILUK_OK;
+}
+
+int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t k,
+                      biluk_plan_t **out, int64_t *err_row) {
+    if (!out) return fail(BILUK_EARG, "null output");
+    *out = nullptr;
+    auto *h = new (std::nothrow) biluk_plan;
+    if (!h) return fail(BILUK_ENOMEM, "out of host memory");
+    int rc = plan_analyse(h->p, bs, n, row_ptr, col_idx, k, err_row);
+    if (rc != BILUK_OK) {
+        delete h;
+        return rc;
+    }
+    int dev = 0, sms = 148, smem = 227 * 1024;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    } else {
+        cudaGetLastError();   // no device here: plan for a B200
+    }
+    plan_layout(h->p, sms, size_t(smem));
+    *out = h;
+    return BILUK_OK;
+}
+
+void biluk_plan_destroy(biluk_plan_t *plan) { delete plan; }
+
+uint64_t biluk_plan_workspace_bytes(const biluk_plan_t *plan) { return plan ? plan->p.off.total : 0; }
+
+int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, void *stream) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    Plan &p = plan->p;
+    if (bytes < p.off.total) return fail(BILUK_EARG, "workspace too small");
+    if (reinterpret_cast<uintptr_t>(dev_workspace) % 256) return fail(BILUK_EARG, "workspace must be 256-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    p.ws = static_cast<unsigned char *>(dev_workspace);
+    // launch configuration check: the persistent sweep needs every CTA resident
+    int per_sm = 0;
+    CUDA_TRY(sweep_occupancy(p, &per_sm), "sweep occupancy");
+    if (per_sm < 1) return fail(BILUK_EUNSUPPORTED, "sweep kernel does not fit on an SM");
+    auto up = [&](uint64_t off, const void *src, size_t n) -> cudaError_t {
+        if (n == 0) return cudaSuccess;
+        return cudaMemcpyAsync(p.ws + off, src, n, cudaMemcpyHostToDevice, s);
+    };
+    CUDA_TRY(up(p.off.p_rp, p.p_rp.data(), 4 * p.p_rp.size()), "upload");
+    CUDA_TRY(up(p.off.p_ci, p.p_ci.data(), 4 * p.p_ci.size()), "upload");
+    CUDA_TRY(up(p.off.p_diag, p.p_diag.data(), 4 * p.p_diag.size()), "upload");
+    CUDA_TRY(up(p.off.a2p, p.a2p.data(), 4 * p.a2p.size()), "upload");
+    CUDA_TRY(up(p.off.forder, p.forder.data(), 4 * p.forder.size()), "upload");
+    CUDA_TRY(up(p.off.sl_rows, p.sl.tile_rows.data(), 4 * p.sl.tile_rows.size()), "upload");
+    CUDA_TRY(up(p.off.sl_meta, p.sl.meta.data(), 8 * p.sl.meta.size()), "upload");
+    CUDA_TRY(up(p.off.su_rows, p.su.tile_rows.data(), 4 * p.su.tile_rows.size()), "upload");
+    CUDA_TRY(up(p.off.su_meta, p.su.meta.data(), 8 * p.su.meta.size()), "upload");
+    // parity-tagged vectors start at parity 0 everywhere; the first apply uses parity 1
+    CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
+    CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
+    DevStatus init{};
+    init.epoch = 1;
+    init.ferr_row = (long long)INT64_MAX;
+    CUDA_TRY(cudaMemcpyAsync(p.ws + p.off.status, &init, sizeof(init), cudaMemcpyHostToDevice, s), "upload");
+    CUDA_TRY(cudaStreamSynchronize(s), "bind sync");
+    p.bound = true;
+    p.factored = false;
+    return BILUK_OK;
+}
+
+int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream, int64_t *err_row) {
+    if (!plan || !plan->p.bound) return fail(BILUK_EARG, "plan is not bound to a workspace");
+    Plan &p = plan->p;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevStatus *st = dev_status(p);
+    {
+        int32_t z[2] = {0, 0};
+        long long big = (long long)INT64_MAX;
+        CUDA_TRY(cudaMemcpyAsync(&st->status, z, sizeof(z), cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemcpyAsync(&st->ferr_row, &big, sizeof(big), cudaMemcpyHostToDevice, s), "status reset");
+    }
+    CUDA_TRY(launch_materialize(p, dev_a_vals, s), "materialize");
+    CUDA_TRY(launch_factor(p, s), "factorize");
+    DevStatus h{};
+    CUDA_TRY(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s), "status read");
+    CUDA_TRY(cudaStreamSynchronize(s), "factorize sync");
+    if (h.fstatus != 0) {
+        p.factored = false;
+        if (err_row) *err_row = h.ferr_row;
+        if (h.fstatus == BILUK_EZEROPIVOT)
+            return fail(BILUK_EZEROPIVOT, "zero pivot at row " + std::to_string(h.ferr_row));
+        return fail(BILUK_ESINGULAR, "singular diagonal block at row " + std::to_string(h.ferr_row));
+    }
+    CUDA_TRY(launch_split(p, s), "split");
+    CUDA_TRY(launch_pack(p, s), "pack");
+    CUDA_TRY(cudaStreamSynchronize(s), "pack sync");
+    p.factored = true;
+    return BILUK_OK;
+}
+
+int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream) {
+    if (!plan || !plan->p.factored) return fail(BILUK_EARG, "plan is not factored");
+    Plan &p = plan->p;
+    if (p.n == 0) return BILUK_OK;
+    if (dev_b == dev_x) return fail(BILUK_EARG, "output may not alias the right-hand side");
+    SweepArgs a{};
+    a.meta_l = reinterpret_cast<const TileMeta *>(p.ws + p.off.sl_meta);
+    a.meta_u = reinterpret_cast<const TileMeta *>(p.ws + p.off.su_meta);
+    a.rec_l = p.ws + p.off.sl_rec;
+    a.rec_u = p.ws + p.off.su_rec;
+    a.nl = p.sl.ntiles;
+    a.nu = p.su.ntiles;
+    a.b = dev_b;
+    a.y_t = reinterpret_cast<double *>(p.ws + p.off.y_t);
+    a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
+    a.out = dev_x;
+    a.st = dev_status(p);
+    a.skip_flag = nullptr;
+    a.stages = p.sweep_stages;
+    a.stage_bytes = int(p.stage_bytes);
+    a.timeout_ns = 2000000000ull;
+    a.backoff_ns = 0;
+    CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+    return BILUK_OK;
+}
+
+int biluk_plan_status(biluk_plan_t *plan, void *stream) {
+    if (!plan || !plan->p.bound) return fail(BILUK_EARG, "plan is not bound");
+    Plan &p = plan->p;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int32_t code = 0;
+    CUDA_TRY(cudaMemcpyAsync(&code, &dev_status(p)->status, 4, cudaMemcpyDeviceToHost, s), "status read");
+    CUDA_TRY(cudaStreamSynchronize(s), "status sync");
+    if (code != 0) {
+        // the tagged vectors are in an unknown state: restart the parity protocol
+        int32_t z = 0;
+        uint32_t one = 1, zero = 0;
+        CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->status, &z, 4, cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->epoch, &one, 4, cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->done_ctas, &zero, 4, cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
+        CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
+        CUDA_TRY(cudaStreamSynchronize(s), "status sync");
+        return fail(code, "device dependency wait timed out in the triangular sweep");
+    }
+    return BILUK_OK;
+}
+
+int biluk_plan_info(const biluk_plan_t *plan, int64_t *info, int32_t ninfo) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    const Plan &p = plan->p;
+    const int64_t v[] = {p.n,          p.bs,         p.k,           p.nnzA,          p.nnzP,
+                         p.nL,         p.nU,         p.nlev_L,      p.nlev_U,        p.sl.ntiles,
+                         p.su.ntiles,  rows_per_tile(p.bs), int64_t(p.off.total), apply_bytes(p), spmv_bytes(p),
+                         p.sweep_ctas, p.sweep_warps, p.sweep_stages, p.stage_bytes,
+                         std::max(p.sl.max_slots, p.su.max_slots)};
+    const int nv = int(sizeof(v) / sizeof(v[0]));
+    for (int i = 0; i < ninfo; ++i) info[i] = i < nv ? v[i] : 0;
+    return BILUK_OK;
+}
+
+int biluk_plan_copy_factors(biluk_plan_t *plan, int64_t *L_row_ptr, int64_t *L_col_idx, double *L_vals, double *dinv,
+                            int64_t *U_row_ptr, int64_t *U_col_idx, double *U_vals, void *stream) {
+    if (!plan || !plan->p.factored) return fail(BILUK_EARG, "plan is not factored");
+    Plan &p = plan->p;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t bs2 = int64_t(p.bs) * p.bs;
+    std::vector<double> pv(size_t(p.nnzP * bs2)), dv(size_t(p.n * bs2));
+    CUDA_TRY(cudaMemcpyAsync(pv.data(), p.ws + p.off.pvals, 8 * pv.size(), cudaMemcpyDeviceToHost, s), "copy");
+    CUDA_TRY(cudaMemcpyAsync(dv.data(), p.ws + p.off.dinv, 8 * dv.size(), cudaMemcpyDeviceToHost, s), "copy");
+    CUDA_TRY(cudaStreamSynchronize(s), "copy sync");
+    int64_t lq = 0, uq = 0;
+    if (L_row_ptr) L_row_ptr[0] = 0;
+    if (U_row_ptr) U_row_ptr[0] = 0;
+    for (int64_t i = 0; i < p.n; ++i) {
+        for (int32_t t = p.p_rp[i]; t < p.p_rp[i + 1]; ++t) {
+            if (t < p.p_diag[i]) {
+                if (L_col_idx) L_col_idx[lq] = p.p_ci[t];
+                if (L_vals) std::memcpy(L_vals + lq * bs2, pv.data() + int64_t(t) * bs2, 8 * bs2);
+                ++lq;
+            } else if (t > p.p_diag[i]) {
+                if (U_col_idx) U_col_idx[uq] = p.p_ci[t];
+                if (U_vals) std::memcpy(U_vals + uq * bs2, pv.data() + int64_t(t) * bs2, 8 * bs2);
+                ++uq;
+            }
+        }
+        if (L_row_ptr) L_row_ptr[i + 1] = lq;
+        if (U_row_ptr) U_row_ptr[i + 1] = uq;
+        if (dinv)   // column-major on the device -> row-major (n, bs, bs)
+            for (int r = 0; r < p.bs; ++r)
+                for (int c = 0; c < p.bs; ++c) dinv[i * bs2 + r * p.bs + c] = dv[i * bs2 + c * p.bs + r];
+    }
+    return BILUK_OK;
+}
+
+int biluk_op_create(int32_t bs, int64_t n_block_rows, int64_t n_block_cols, const int64_t *row_ptr,
+                    const int64_t *col_idx, biluk_op_t **out) {
+    if (!out) return fail(BILUK_EARG, "null output");
+    *out = nullptr;
+    auto *h = new (std::nothrow) biluk_op;
+    if (!h) return fail(BILUK_ENOMEM, "out of host memory");
+    int rc = op_analyse(h->o, bs, n_block_rows, n_block_cols, row_ptr, col_idx);
+    if (rc != BILUK_OK) {
+        delete h;
+        return rc;
+    }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    else
+        cudaGetLastError();
+    h->o.num_sms = sms;
+    *out = h;
+    return BILUK_OK;
+}
+
+void biluk_op_destroy(biluk_op_t *op) { delete op; }
+
+uint64_t biluk_op_workspace_bytes(const biluk_op_t *op) { return op ? op->o.off.total : 0; }
+
+int biluk_op_bind(biluk_op_t *op, void *dev_workspace, uint64_t bytes, void *stream) {
+    if (!op) return fail(BILUK_EARG, "null operator");
+    Op &o = op->o;
+    if (bytes < o.off.total) return fail(BILUK_EARG, "workspace too small");
+    if (reinterpret_cast<uintptr_t>(dev_workspace) % 256) return fail(BILUK_EARG, "workspace must be 256-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    o.ws = static_cast<unsigned char *>(dev_workspace);
+    if (o.rp.size()) CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.rp, o.rp.data(), 4 * o.rp.size(), cudaMemcpyHostToDevice, s), "upload");
+    if (o.ci.size()) CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.ci, o.ci.data(), 4 * o.ci.size(), cudaMemcpyHostToDevice, s), "upload");
+    if (o.meta.size())
+        CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.meta, o.meta.data(), 8 * o.meta.size(), cudaMemcpyHostToDevice, s), "upload");
+    CUDA_TRY(cudaStreamSynchronize(s), "bind sync");
+    o.bound = true;
+    o.valued = false;
+    return BILUK_OK;
+}
+
+int biluk_op_set_values(biluk_op_t *op, const double *dev_vals, void *stream) {
+    if (!op || !op->o.bound) return fail(BILUK_EARG, "operator is not bound to a workspace");
+    CUDA_TRY(launch_pack_ell(op->o, dev_vals, static_cast<cudaStream_t>(stream)), "pack");
+    op->o.valued = true;
+    return BILUK_OK;
+}
+
+int biluk_op_spmv(biluk_op_t *op, const double *dev_x, double *dev_y, void *stream) {
+    if (!op || !op->o.valued) return fail(BILUK_EARG, "operator has no values");
+    if (op->o.n == 0) return BILUK_OK;
+    CUDA_TRY(launch_spmv(op->o, dev_x, dev_y, nullptr, static_cast<cudaStream_t>(stream)), "spmv");
+    return BILUK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,38 @@
+// Kernel launch interface used by the C ABI (abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "biluk_internal.h"
+
+namespace biluk {
+
+struct SweepArgs {
+    const TileMeta *meta_l;
+    const TileMeta *meta_u;
+    const unsigned char *rec_l;
+    const unsigned char *rec_u;
+    int64_t nl, nu;          // tiles of the L and U' sweeps
+    const double *b;         // right-hand side (n*bs)
+    double *y_t;             // parity-tagged intermediate y
+    double *x_t;             // parity-tagged result x (dependency copy)
+    double *out;             // untagged result (may be null)
+    DevStatus *st;
+    const int *skip_flag;    // when non-null and *skip_flag != 0 the launch is a no-op
+    int stages;
+    int stage_bytes;
+    uint64_t timeout_ns;
+    int backoff_ns;
+};
+
+cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);
+cudaError_t launch_factor(const Plan &p, cudaStream_t s);
+cudaError_t launch_split(const Plan &p, cudaStream_t s);
+cudaError_t launch_pack(const Plan &p, cudaStream_t s);
+cudaError_t launch_pack_ell(const Op &o, const double *avals, cudaStream_t s);
+cudaError_t launch_sweep(const Plan &p, const SweepArgs &a, cudaStream_t s);
+cudaError_t sweep_occupancy(const Plan &p, int *blocks_per_sm);
+size_t sweep_smem_bytes(const Plan &p);
+cudaError_t launch_spmv(const Op &o, const double *x, double *y, const int *skip, cudaStream_t s);
+
+}  // namespace biluk

@@ -1,0 +1,283 @@
+"""Host-side sparse containers of the drop-in API (reference sparse.py).
+
+Same constructors, fields, validation rules and layouts as the reference
+(`CsrMatrix` sparse.py:55-89, `BcsrMatrix` :92-151 with column-major blocks,
+`PatternMatrix` :154-221), so objects can be passed back and forth.  These
+are index/value holders only: every numeric operation on the path runs on the
+GPU through libbiluk.  Reference objects are accepted anywhere through
+duck typing (``as_bsr``).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import StructuralError
+
+__all__ = ["CsrMatrix", "BcsrMatrix", "PatternMatrix", "bcsr_from_csr", "csr_expand",
+           "extract_point_pattern", "csr_from_triplets", "as_bsr"]
+
+
+def _index_array(a, name):
+    arr = np.ascontiguousarray(a, dtype=np.int64)
+    if arr.ndim != 1:
+        raise StructuralError(f"{name} must be one-dimensional")
+    return arr
+
+
+def _check_structure(nrows, ncols, rp, ci, what):
+    """Structural invariants of CSR / BSR indices (reference sparse.py:35-52)."""
+    if nrows < 0 or ncols < 0:
+        raise StructuralError(f"{what}: negative dimension")
+    if rp.shape != (nrows + 1,) or rp[0] != 0:
+        raise StructuralError(f"{what}: row_ptr must have num_rows+1 entries starting at 0")
+    if np.any(np.diff(rp) < 0):
+        raise StructuralError(f"{what}: row_ptr must be nondecreasing")
+    nnz = int(rp[-1])
+    if ci.shape != (nnz,):
+        raise StructuralError(f"{what}: col_idx length must equal row_ptr[-1]")
+    if nnz:
+        if ci.min() < 0 or ci.max() >= ncols:
+            raise StructuralError(f"{what}: column index out of range")
+        row_start = np.zeros(nnz + 1, dtype=bool)
+        row_start[rp[:-1]] = True
+        if np.any((np.diff(ci) <= 0) & ~row_start[1:nnz]):
+            raise StructuralError(f"{what}: column indices must increase strictly within a row")
+
+
+class CsrMatrix:
+    """Point-wise CSR matrix (reference sparse.py:55-89)."""
+
+    def __init__(self, num_rows, num_cols, row_ptr, col_idx, values):
+        self.num_rows = int(num_rows)
+        self.num_cols = int(num_cols)
+        self.row_ptr = _index_array(row_ptr, "row_ptr")
+        self.col_idx = _index_array(col_idx, "col_idx")
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        _check_structure(self.num_rows, self.num_cols, self.row_ptr, self.col_idx, "CsrMatrix")
+        if self.values.shape != self.col_idx.shape:
+            raise StructuralError("CsrMatrix: values length must equal col_idx length")
+
+    @property
+    def shape(self):
+        return (self.num_rows, self.num_cols)
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+    def row(self, i):
+        s, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        return self.col_idx[s:e], self.values[s:e]
+
+    def to_dense(self):
+        out = np.zeros(self.shape)
+        rows = np.repeat(np.arange(self.num_rows), np.diff(self.row_ptr))
+        out[rows, self.col_idx] = self.values
+        return out
+
+    def __repr__(self):
+        return f"CsrMatrix({self.num_rows}x{self.num_cols}, nnz={self.nnz})"
+
+
+class BcsrMatrix:
+    """Block CSR with dense bs x bs blocks flattened column-major (reference sparse.py:92-151)."""
+
+    def __init__(self, block_size, num_block_rows, num_block_cols, row_ptr, col_idx, values):
+        self.block_size = int(block_size)
+        self.num_block_rows = int(num_block_rows)
+        self.num_block_cols = int(num_block_cols)
+        self.row_ptr = _index_array(row_ptr, "row_ptr")
+        self.col_idx = _index_array(col_idx, "col_idx")
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if self.block_size < 1:
+            raise StructuralError("BcsrMatrix: block size must be at least 1")
+        _check_structure(self.num_block_rows, self.num_block_cols, self.row_ptr, self.col_idx, "BcsrMatrix")
+        if self.values.shape != (self.nnzb * self.block_size ** 2,):
+            raise StructuralError("BcsrMatrix: values length must be nnzb * block_size^2")
+
+    @property
+    def nnzb(self):
+        return int(self.row_ptr[-1])
+
+    @property
+    def shape(self):
+        return (self.num_block_rows * self.block_size, self.num_block_cols * self.block_size)
+
+    @property
+    def blocks(self):
+        """(nnzb, bs, bs) view; element [t, r, c] is row r, column c of block t."""
+        bs = self.block_size
+        return self.values.reshape(self.nnzb, bs, bs).swapaxes(1, 2)
+
+    def block_row(self, i):
+        s, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        return self.col_idx[s:e], s
+
+    def to_dense(self):
+        bs = self.block_size
+        out = np.zeros(self.shape)
+        brow = np.repeat(np.arange(self.num_block_rows), np.diff(self.row_ptr))
+        r = np.arange(bs)
+        rows = (brow[:, None, None] * bs + r[None, :, None])
+        cols = (self.col_idx[:, None, None] * bs + r[None, None, :])
+        out[rows, cols] = self.blocks
+        return out
+
+    def __repr__(self):
+        return (f"BcsrMatrix(bs={self.block_size}, {self.num_block_rows}x{self.num_block_cols} blocks, "
+                f"nnzb={self.nnzb})")
+
+
+class PatternMatrix:
+    """Value-free square pattern with sorted rows (reference sparse.py:154-221)."""
+
+    def __init__(self, n, rows=None):
+        self.n = int(n)
+        if self.n < 0:
+            raise StructuralError("PatternMatrix: negative dimension")
+        if rows is None:
+            self.rows = [[] for _ in range(self.n)]
+            return
+        rows = [[int(j) for j in r] for r in rows]
+        if len(rows) != self.n:
+            raise StructuralError("PatternMatrix: need one row list per row")
+        for i, r in enumerate(rows):
+            if any(r[t] >= r[t + 1] for t in range(len(r) - 1)):
+                raise StructuralError(f"PatternMatrix: row {i} is not strictly increasing")
+            if r and (r[0] < 0 or r[-1] >= self.n):
+                raise StructuralError(f"PatternMatrix: row {i} has an index out of range")
+        self.rows = rows
+
+    @classmethod
+    def from_csr_arrays(cls, n, rp, ci):
+        out = cls(n)
+        rp = np.asarray(rp)
+        ci = np.asarray(ci)
+        out.rows = [ci[rp[i]:rp[i + 1]].tolist() for i in range(n)]
+        return out
+
+    def to_csr_arrays(self):
+        rp = np.zeros(self.n + 1, dtype=np.int64)
+        rp[1:] = np.cumsum([len(r) for r in self.rows])
+        ci = np.fromiter((j for r in self.rows for j in r), dtype=np.int64, count=int(rp[-1]))
+        return rp, ci
+
+    @property
+    def row_lengths(self):
+        return [len(r) for r in self.rows]
+
+    @property
+    def nnz(self):
+        return sum(len(r) for r in self.rows)
+
+    def as_set(self):
+        return {(i, j) for i, r in enumerate(self.rows) for j in r}
+
+    def __eq__(self, other):
+        if not hasattr(other, "rows") or not hasattr(other, "n"):
+            return NotImplemented
+        return self.n == other.n and self.rows == other.rows
+
+    def __repr__(self):
+        return f"PatternMatrix(n={self.n}, nnz={self.nnz})"
+
+
+def csr_from_triplets(num_rows, num_cols, entries):
+    """CSR from (row, col, value) triplets, duplicates summed (reference sparse.py:248-258)."""
+    entries = list(entries)
+    if not entries:
+        return CsrMatrix(num_rows, num_cols, np.zeros(num_rows + 1, np.int64), [], [])
+    r, c, v = (np.asarray(x) for x in zip(*entries))
+    r = r.astype(np.int64)
+    c = c.astype(np.int64)
+    v = v.astype(np.float64)
+    if r.min() < 0 or r.max() >= num_rows or c.min() < 0 or c.max() >= num_cols:
+        raise StructuralError("triplet index outside the matrix")
+    key = r * num_cols + c
+    order = np.argsort(key, kind="stable")
+    key, v = key[order], v[order]
+    uniq, first = np.unique(key, return_index=True)
+    vals = np.add.reduceat(v, first)
+    rows = uniq // num_cols
+    rp = np.zeros(num_rows + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=num_rows), out=rp[1:])
+    return CsrMatrix(num_rows, num_cols, rp, uniq % num_cols, vals)
+
+
+def bcsr_from_csr(a, bs):
+    """Reblock a point CSR matrix into bs x bs blocks (reference sparse.py:304-334)."""
+    bs = int(bs)
+    if bs < 1:
+        raise StructuralError("block size must be at least 1")
+    if a.num_rows % bs or a.num_cols % bs:
+        raise StructuralError(f"block size {bs} does not divide matrix shape {a.num_rows}x{a.num_cols}")
+    nbr, nbc = a.num_rows // bs, a.num_cols // bs
+    if a.row_ptr[-1] == 0:
+        return BcsrMatrix(bs, nbr, nbc, np.zeros(nbr + 1, np.int64), [], [])
+    erow = np.repeat(np.arange(a.num_rows, dtype=np.int64), np.diff(a.row_ptr))
+    col = np.asarray(a.col_idx, dtype=np.int64)
+    key = (erow // bs) * nbc + col // bs
+    uniq = np.unique(key)
+    rp = np.zeros(nbr + 1, np.int64)
+    np.cumsum(np.bincount(uniq // nbc, minlength=nbr), out=rp[1:])
+    vals = np.zeros(uniq.size * bs * bs)
+    slot = np.searchsorted(uniq, key)
+    vals[slot * bs * bs + (col % bs) * bs + (erow % bs)] = a.values
+    return BcsrMatrix(bs, nbr, nbc, rp, uniq % nbc, vals)
+
+
+def csr_expand(a):
+    """Point CSR of a block matrix with exact zeros dropped (reference sparse.py:337-374).
+
+    Within point row (I, r) the entries follow block order, then the in-block
+    column, as in the reference.
+    """
+    bs = int(a.block_size)
+    n, m = int(a.num_block_rows), int(a.num_block_cols)
+    rp = np.asarray(a.row_ptr, dtype=np.int64)
+    ci = np.asarray(a.col_idx, dtype=np.int64)
+    nnzb = int(rp[-1])
+    blk = np.asarray(a.values, dtype=np.float64).reshape(nnzb, bs, bs)   # [slot][c][r]
+    brow = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    # order (block row, r, slot, c): slots of a block row are contiguous
+    vals = blk.transpose(0, 2, 1)                                       # [slot][r][c]
+    # per block row: (r, slot, c) ordering = transpose of (slot, r, c) inside the row
+    order = np.lexsort((np.tile(np.arange(bs), nnzb * bs),
+                        np.repeat(np.arange(nnzb), bs * bs),
+                        np.tile(np.repeat(np.arange(bs), bs), nnzb),
+                        np.repeat(brow, bs * bs)))
+    v = vals.reshape(-1)[order]
+    cols = (np.repeat(ci, bs * bs) * bs + np.tile(np.arange(bs), nnzb * bs))[order]
+    prow = (np.repeat(brow, bs * bs) * bs + np.tile(np.repeat(np.arange(bs), bs), nnzb))[order]
+    keep = v != 0.0
+    v, cols, prow = v[keep], cols[keep], prow[keep]
+    prp = np.zeros(n * bs + 1, np.int64)
+    np.cumsum(np.bincount(prow, minlength=n * bs), out=prp[1:])
+    return CsrMatrix(n * bs, m * bs, prp, cols, v)
+
+
+def extract_point_pattern(a):
+    """Pattern of the stored (block) structure; values never read (reference sparse.py:261-275)."""
+    if hasattr(a, "block_size"):
+        n, m = a.num_block_rows, a.num_block_cols
+    else:
+        n, m = a.num_rows, a.num_cols
+    if n != m:
+        raise StructuralError("pattern extraction requires a square matrix")
+    return PatternMatrix.from_csr_arrays(n, a.row_ptr, a.col_idx)
+
+
+def as_bsr(a):
+    """(bs, n_rows, n_cols, row_ptr int64, col_idx int64, values f64) of any BSR/CSR-like object.
+
+    A point CSR matrix is block size one (reference factor.py:312-313).
+    """
+    if hasattr(a, "block_size"):
+        return (int(a.block_size), int(a.num_block_rows), int(a.num_block_cols),
+                np.ascontiguousarray(a.row_ptr, dtype=np.int64), np.ascontiguousarray(a.col_idx, dtype=np.int64),
+                np.ascontiguousarray(a.values, dtype=np.float64))
+    if hasattr(a, "num_rows"):
+        return (1, int(a.num_rows), int(a.num_cols), np.ascontiguousarray(a.row_ptr, dtype=np.int64),
+                np.ascontiguousarray(a.col_idx, dtype=np.int64), np.ascontiguousarray(a.values, dtype=np.float64))
+    raise TypeError("expected a BcsrMatrix or CsrMatrix")

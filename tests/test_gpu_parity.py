@@ -1,0 +1,170 @@
+"""GPU parity of the CUDA path against the reference (golden vectors) and the oracle.
+
+Bars (BASELINE.json north star): patterns and level sets exact; L / D^-1 / U'
+and preconditioned vectors within 1e-12 relative (max-norm, acceptance-01
+style); Krylov iteration counts within +-1.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_files, load_golden, rel_err
+from oracle import iluk_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_files()
+IDS = [os.path.basename(p)[:-4] for p in CASES]
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def b2(cuda_ok):
+    import paper_1703_01325_b200 as mod
+    return mod
+
+
+def _golden_matrix(b2, g):
+    n, bs = int(g["n"]), int(g["bs"])
+    return b2.BcsrMatrix(bs, n, n, g["rp"], g["ci"], g["vals"])
+
+
+@pytest.mark.parametrize("path", CASES, ids=IDS)
+def test_factors_apply_and_solvers_match_reference(b2, path):
+    g = load_golden(path)
+    k = int(g["k"])
+    a = _golden_matrix(b2, g)
+    f = b2.build_preconditioner(a, k)
+    # factors: structure exact, values 1e-12
+    assert np.array_equal(f.L.row_ptr, g["L_rp"]) and np.array_equal(f.L.col_idx, g["L_ci"])
+    assert np.array_equal(f.uprime.row_ptr, g["U_rp"]) and np.array_equal(f.uprime.col_idx, g["U_ci"])
+    assert rel_err(f.L.values, g["L_vals"]) <= TOL
+    assert rel_err(f.uprime.values, g["U_vals"]) <= TOL
+    assert rel_err(f.dinv, g["dinv"]) <= TOL
+    # point-wise schedules on the zero-dropped expansions: exact
+    assert np.array_equal(f.lower_schedule.level_of_row, g["lo_level_of_row"])
+    assert np.array_equal(f.upper_schedule.level_of_row, g["up_level_of_row"])
+    # preconditioned vector
+    z = b2.apply_preconditioner(f, g["rhs"])
+    assert rel_err(z, g["apply_out"]) <= TOL
+    # SpMV
+    ax = b2.spmv(a, np.ones(a.shape[0]))
+    absax = orc.bsr_spmv(a.num_block_rows, a.block_size, g["rp"], g["ci"], np.abs(g["vals"]), np.ones(a.shape[0]))
+    assert np.abs(ax - g["spmv_ones"]).max() <= 1e-14 * absax.max()
+    # Krylov: iteration counts within +-1 and the same verdict
+    b = g["spmv_ones"]
+    x, st = b2.gmres(a, b, M=f, cfg=b2.SolverConfig(restart=30, rel_tol=1e-6))
+    assert abs(st.iterations - int(g["gmres_iters"])) <= 1
+    assert st.converged == bool(g["gmres_conv"])
+    x, st = b2.bicgstab(a, b, M=f, cfg=b2.SolverConfig(rel_tol=1e-6))
+    assert abs(st.iterations - int(g["bicg_iters"])) <= 1
+    assert st.converged == bool(g["bicg_conv"])
+
+
+@pytest.mark.parametrize("nx,bs,k", [(16, 3, 0), (12, 3, 2), (10, 4, 1), (8, 8, 1), (9, 2, 3), (7, 5, 2)])
+def test_synthetic_vs_oracle(b2, nx, bs, k):
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, bs, seed=11)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    f = b2.build_preconditioner(a, k)
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, k)
+    assert rel_err(f.L.values, of.L_vals) <= TOL
+    assert rel_err(f.uprime.values, of.U_vals) <= TOL
+    assert rel_err(f.dinv, of.dinv) <= TOL
+    rhs = np.random.default_rng(1).standard_normal(n * bs)
+    assert rel_err(b2.apply_preconditioner(f, rhs), of.apply(rhs)) <= TOL
+
+
+def test_apply_is_deterministic_and_async_torch_path(b2):
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(24, 20, 16, 3, seed=2)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 1)
+    rhs = torch.randn(n * bs, dtype=torch.float64, device="cuda")
+    x1 = b2.apply_preconditioner(f, rhs)
+    outs = [b2.apply_preconditioner(f, rhs) for _ in range(5)]
+    f.status()
+    for x in outs:
+        assert torch.equal(x, x1)           # bitwise repeatable run to run
+    xh = b2.apply_preconditioner(f, rhs.cpu().numpy())
+    assert np.array_equal(xh, x1.cpu().numpy())
+    # linearity to rounding
+    r2 = torch.randn_like(rhs)
+    lhs = b2.apply_preconditioner(f, 3.0 * rhs + r2)
+    rhs_lin = 3.0 * x1 + b2.apply_preconditioner(f, r2)
+    assert float((lhs - rhs_lin).abs().max() / rhs_lin.abs().max()) <= 1e-13
+
+
+def test_factorization_errors_match_reference(b2):
+    # singular leading block -> SingularBlockError with .row == 0 (reference test_factor.py:145-155)
+    dense = np.zeros((4, 4))
+    dense[:2, :2] = [[1.0, 2.0], [2.0, 4.0]]
+    dense[2:, 2:] = np.eye(2)
+    dense[2:, :2] = np.eye(2)
+    trip = [(i, j, dense[i, j]) for i in range(4) for j in range(4) if dense[i, j] != 0.0 or i // 2 == j // 2]
+    a = b2.bcsr_from_csr(b2.csr_from_triplets(4, 4, trip), 2)
+    with pytest.raises(b2.SingularBlockError) as exc:
+        b2.build_preconditioner(a, 0)
+    assert exc.value.row == 0 and str(exc.value).startswith("factorize:")
+    # zero pivot on the scalar path -> FactorizationError, row 0 (test_factor.py:190-203)
+    a = b2.csr_from_triplets(2, 2, [(0, 0, 0.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 1.0)])
+    with pytest.raises(b2.FactorizationError) as exc:
+        b2.build_preconditioner(a, 0)
+    assert exc.value.row == 0 and str(exc.value).startswith("factorize:")
+    # missing diagonal surfaces from the symbolic stage by name
+    a = b2.csr_from_triplets(2, 2, [(0, 1, 1.0), (1, 0, 1.0)])
+    with pytest.raises(b2.StructuralError) as exc:
+        b2.build_preconditioner(a, 0)
+    assert str(exc.value).startswith("symbolic-phase:")
+    # singular block deeper in the matrix: the FIRST failing row is reported
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(6, 5, 4, 3, seed=1)
+    vals = vals.copy()
+    for row in (77, 31):      # an all-zero block row factors to an all-zero U_ii
+        vals[rp[row] * 9:rp[row + 1] * 9] = 0.0
+    with pytest.raises(b2.SingularBlockError) as exc:
+        b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0)
+    assert exc.value.row == 31
+
+
+def test_bad_lengths_and_callable_preconditioner(b2):
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(6, 6, 6, 3, seed=4)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    f = b2.build_preconditioner(a, 1)
+    with pytest.raises(ValueError):
+        b2.apply_preconditioner(f, np.zeros(n * bs - 1))
+    b = b2.spmv(a, np.ones(n * bs))
+    # the reference idiom: an opaque callable M (gmres.py:85-87)
+    x1, s1 = b2.gmres(a, b, M=lambda v: b2.apply_preconditioner(f, v), cfg=b2.SolverConfig(restart=30))
+    x2, s2 = b2.gmres(a, b, M=f, cfg=b2.SolverConfig(restart=30))
+    assert s1.iterations == s2.iterations and s1.converged and s2.converged
+    assert np.allclose(x1, x2, rtol=0, atol=1e-12)
+    assert np.allclose(x2, 1.0, atol=1e-4)
+    _, s0 = b2.gmres(a, b, cfg=b2.SolverConfig(restart=30))
+    assert s0.iterations > s2.iterations          # preconditioning helps
+    with pytest.raises(ValueError):
+        b2.gmres(a, np.zeros(n * bs + 1))
+
+
+def test_gmres_known_answers(b2):
+    # identity converges in one iteration (reference test_gmres.py:13-20)
+    a = b2.csr_from_triplets(10, 10, [(i, i, 1.0) for i in range(10)])
+    b = np.arange(1.0, 11.0)
+    x, st = b2.gmres(a, b)
+    assert st.converged and st.iterations == 1 and np.allclose(x, b, atol=1e-12)
+    # zero rhs short-circuits
+    x, st = b2.gmres(a, np.zeros(10))
+    assert st.converged and st.iterations == 0 and not x.any()
+    # iteration cap reported honestly
+    from paper_1703_01325_b200.synthetic import poisson7_pattern
+    rp, ci = poisson7_pattern(10, 10, 1)
+    vals = np.where(ci == np.repeat(np.arange(100), np.diff(rp)), 6.0, -1.0)
+    p = b2.CsrMatrix(100, 100, rp, ci, vals)
+    x, st = b2.gmres(p, b2.spmv(p, np.ones(100)), cfg=b2.SolverConfig(max_iters=3, rel_tol=1e-14))
+    assert not st.converged and st.iterations == 3
+    # full pattern ILU(n) is exact LU: one preconditioned iteration (acceptance 09)
+    rng = np.random.default_rng(909)
+    dense = rng.standard_normal((20, 20)) + 20 * np.eye(20)
+    a = b2.csr_from_triplets(20, 20, [(i, j, dense[i, j]) for i in range(20) for j in range(20)])
+    f = b2.build_preconditioner(b2.bcsr_from_csr(a, 1), 20)
+    _, st = b2.gmres(a, a.to_dense() @ rng.standard_normal(20), M=f)
+    assert st.converged and st.iterations == 1
