@@ -109,6 +109,13 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
  * Asynchronous; a dependency-wait timeout is reported by biluk_plan_status. */
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream);
 
+/* Runtime knobs of the sweep kernel (no effect on results):
+ *   "gap"             fine-grained dependency polling starts when every level
+ *                     <= (tile level - gap) is complete (default 2)
+ *   "coarse_sleep_ns" back-off of the per-warp progress poll (default 64)
+ *   "fine_sleep_ns"   back-off of the per-value dependency poll (default 0) */
+int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value);
+
 /* Synchronises the stream and returns the sticky device status of the plan
  * (BILUK_OK or BILUK_ETIMEOUT), clearing it. */
 int biluk_plan_status(biluk_plan_t *plan, void *stream);

@@ -153,9 +153,11 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     CUDA_TRY(up(p.off.a2p, p.a2p.data(), 4 * p.a2p.size()), "upload");
     CUDA_TRY(up(p.off.forder, p.forder.data(), 4 * p.forder.size()), "upload");
     CUDA_TRY(up(p.off.sl_rows, p.sl.tile_rows.data(), 4 * p.sl.tile_rows.size()), "upload");
-    CUDA_TRY(up(p.off.sl_meta, p.sl.meta.data(), 8 * p.sl.meta.size()), "upload");
+    CUDA_TRY(up(p.off.sl_meta, p.sl.meta.data(), sizeof(TileMeta) * p.sl.meta.size()), "upload");
     CUDA_TRY(up(p.off.su_rows, p.su.tile_rows.data(), 4 * p.su.tile_rows.size()), "upload");
-    CUDA_TRY(up(p.off.su_meta, p.su.meta.data(), 8 * p.su.meta.size()), "upload");
+    CUDA_TRY(up(p.off.su_meta, p.su.meta.data(), sizeof(TileMeta) * p.su.meta.size()), "upload");
+    CUDA_TRY(up(p.off.lvl_tiles, p.lvl_tiles.data(), 4 * p.lvl_tiles.size()), "upload");
+    CUDA_TRY(cudaMemsetAsync(p.ws + p.off.lvl_cnt, 0, 4 * p.lvl_tiles.size(), s), "memset");
     // parity-tagged vectors start at parity 0 everywhere; the first apply uses parity 1
     CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
     CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
@@ -220,8 +222,25 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.stages = p.sweep_stages;
     a.stage_bytes = int(p.stage_bytes);
     a.timeout_ns = 2000000000ull;
-    a.backoff_ns = 0;
+    a.lvl_tiles = reinterpret_cast<const uint32_t *>(p.ws + p.off.lvl_tiles);
+    a.lvl_cnt = reinterpret_cast<uint32_t *>(p.ws + p.off.lvl_cnt);
+    a.nlev_l = p.nlev_L;
+    a.nlev_total = p.nlev_L + p.nlev_U;
+    a.gap = p.tune.gap;
+    a.coarse_sleep_ns = p.tune.coarse_sleep_ns;
+    a.fine_sleep_ns = p.tune.fine_sleep_ns;
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+    return BILUK_OK;
+}
+
+int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value) {
+    if (!plan || !key) return fail(BILUK_EARG, "null argument");
+    SweepTune &t = plan->p.tune;
+    const std::string k(key);
+    if (k == "gap") t.gap = int(value);
+    else if (k == "coarse_sleep_ns") t.coarse_sleep_ns = int(value);
+    else if (k == "fine_sleep_ns") t.fine_sleep_ns = int(value);
+    else return fail(BILUK_EARG, "unknown tuning key " + k);
     return BILUK_OK;
 }
 
@@ -239,6 +258,8 @@ int biluk_plan_status(biluk_plan_t *plan, void *stream) {
         CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->status, &z, 4, cudaMemcpyHostToDevice, s), "status reset");
         CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->epoch, &one, 4, cudaMemcpyHostToDevice, s), "status reset");
         CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->done_ctas, &zero, 4, cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->prefix, &zero, 4, cudaMemcpyHostToDevice, s), "status reset");
+        CUDA_TRY(cudaMemsetAsync(p.ws + p.off.lvl_cnt, 0, 4 * p.lvl_tiles.size(), s), "memset");
         CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
         CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
         CUDA_TRY(cudaStreamSynchronize(s), "status sync");
@@ -329,7 +350,9 @@ int biluk_op_bind(biluk_op_t *op, void *dev_workspace, uint64_t bytes, void *str
     if (o.rp.size()) CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.rp, o.rp.data(), 4 * o.rp.size(), cudaMemcpyHostToDevice, s), "upload");
     if (o.ci.size()) CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.ci, o.ci.data(), 4 * o.ci.size(), cudaMemcpyHostToDevice, s), "upload");
     if (o.meta.size())
-        CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.meta, o.meta.data(), 8 * o.meta.size(), cudaMemcpyHostToDevice, s), "upload");
+        CUDA_TRY(cudaMemcpyAsync(o.ws + o.off.meta, o.meta.data(), sizeof(TileMeta) * o.meta.size(),
+                                 cudaMemcpyHostToDevice, s),
+                 "upload");
     CUDA_TRY(cudaStreamSynchronize(s), "bind sync");
     o.bound = true;
     o.valued = false;

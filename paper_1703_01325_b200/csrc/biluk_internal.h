@@ -57,9 +57,11 @@ BILUK_HD constexpr inline int64_t ell_bytes(int bs, int S) {
     return align128(ell_vals_off(bs, S) + int64_t(S) * bs * bs * rows_per_tile(bs) * 8);
 }
 
-struct TileMeta {      // 8 bytes
+struct TileMeta {      // 16 bytes
     uint32_t off128;   // record offset in 128-byte units
     int32_t nslot;     // S
+    int32_t level;     // 1-based dependency level of the tile's rows (sweeps only)
+    int32_t pad;
 };
 
 // device status block (lives in the workspace)
@@ -69,9 +71,15 @@ struct DevStatus {
     long long ferr_row;      // first failing block row (atomicMin)
     uint32_t epoch;          // apply epoch; parity tag of the sweep vectors
     uint32_t done_ctas;      // CTAs finished in the current sweep launch
-    uint32_t spin_max_lo;    // diagnostics: longest wait seen (ns, low bits)
+    uint32_t prefix;         // every combined level <= prefix is complete (progress hint)
     uint32_t pad0;
-    double scal[64];         // Krylov scalars
+};
+
+// runtime knobs of the sweep (biluk_plan_tune)
+struct SweepTune {
+    int gap = 2;             // fine-grained polling starts once prefix >= level - gap
+    int coarse_sleep_ns = 64;
+    int fine_sleep_ns = 0;
 };
 
 struct Sweep {                       // host copy of one sweep's tile layout
@@ -98,6 +106,8 @@ struct Plan {
     std::vector<int64_t> fptr;       // level pointers into forder (nlev_L + 1)
     int32_t max_row_len = 0;         // longest P' row (factor shared memory)
     Sweep sl, su;                    // L sweep, U' sweep
+    std::vector<uint32_t> lvl_tiles; // tiles per combined level (L levels, then U' levels), 1-based
+    SweepTune tune;
     // launch configuration of the sweep kernel
     int32_t sweep_ctas = 0, sweep_warps = 0, sweep_stages = 0;
     int64_t stage_bytes = 0;
@@ -105,7 +115,7 @@ struct Plan {
     // workspace layout (byte offsets)
     struct {
         uint64_t p_rp, p_ci, p_diag, a2p, forder, pvals, dinv, sl_rows, sl_meta, sl_rec, su_rows, su_meta,
-            su_rec, y_t, x_t, status, total;
+            su_rec, y_t, x_t, lvl_tiles, lvl_cnt, status, total;
     } off{};
     // bound device pointers
     unsigned char *ws = nullptr;

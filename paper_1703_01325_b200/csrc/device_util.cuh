@@ -51,6 +51,11 @@ __device__ __forceinline__ double tag(double v, uint32_t par) {
 __device__ __forceinline__ uint32_t tag_of(double v) {
     return static_cast<uint32_t>(__double_as_longlong(v)) & 1u;
 }
+// consumers clear the tag bit, so what they compute with does not depend on
+// the epoch's parity: results are bitwise identical from apply to apply
+__device__ __forceinline__ double untag(double v) {
+    return __longlong_as_double(__double_as_longlong(v) & ~1ll);
+}
 
 // ---- mbarrier + bulk async copy (cp.async.bulk, the 1-D TMA path)
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {

@@ -323,37 +323,77 @@ __global__ void pack_ell_kernel(int64_t n, int64_t ntiles, const TileMeta *__res
 // chain; only the vector values travel along it.  A lane owns one block row:
 //   L :  y_i = b_i - sum_j L_ij y_j
 //   U':  x_i = D_i^-1 y_i - sum_j U'_ij x_j
-// Dependencies are polled directly on the parity-tagged values (see tag()).
+// Dependencies are polled directly on the parity-tagged values (see tag()),
+// ONE component per dependency until it is published, then the rest.  To keep
+// the polls from flooding L2, a warp first waits (one load per warp, with
+// back-off) until every level <= its own level - gap is complete: per-level
+// tile counters advance a `prefix` of completed levels (a progress hint only;
+// correctness rests on the value tags).
 // ===========================================================================
+__device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const SweepArgs &a) {
+    ++spins;
+    if (spins == 1) {
+        t0 = globaltimer();
+    } else if ((spins & 255u) == 0) {
+        if (globaltimer() - t0 > a.timeout_ns || ld_relaxed_s32(&a.st->status) != 0) {
+            atomicCAS(&a.st->status, 0, int(BILUK_ETIMEOUT));
+            return true;
+        }
+    }
+    return false;
+}
+
+// load the BS components of each pending dependency, values untagged
 template <int BS, int CH>
 __device__ __forceinline__ void wait_values(const double *__restrict__ src, const int (&jj)[CH], double (&xv)[CH][BS],
                                             uint32_t pend, uint32_t par, const SweepArgs &a) {
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    while (true) {
+    // phase 1: poll the last component of every pending dependency
+    uint32_t todo = pend;
+    while (todo) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            if (todo & (1u << c)) {
+                const double v = ld_relaxed(src + int64_t(jj[c]) * BS + (BS - 1));
+                if (tag_of(v) == par) todo &= ~(1u << c);
+            }
+        }
+        if (!todo) break;
+        if (timed_out(t0, spins, a)) return;
+        if (a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
+    }
+    // phase 2: all components (already published in practice; re-poll if not)
+    while (pend) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             if (pend & (1u << c)) {
                 uint32_t ok = 1;
 #pragma unroll
                 for (int q = 0; q < BS; ++q) {
-                    xv[c][q] = ld_relaxed(src + int64_t(jj[c]) * BS + q);
-                    ok &= (tag_of(xv[c][q]) == par);
+                    const double v = ld_relaxed(src + int64_t(jj[c]) * BS + q);
+                    ok &= (tag_of(v) == par);
+                    xv[c][q] = untag(v);
                 }
                 if (ok) pend &= ~(1u << c);
             }
         }
         if (!pend) break;
-        ++spins;
-        if (spins == 1) {
-            t0 = globaltimer();
-        } else if ((spins & 255u) == 0) {
-            if (globaltimer() - t0 > a.timeout_ns || ld_relaxed_s32(&a.st->status) != 0) {
-                atomicCAS(&a.st->status, 0, int(BILUK_ETIMEOUT));
-                break;
-            }
-        }
-        if (a.backoff_ns) __nanosleep(a.backoff_ns);
+        if (timed_out(t0, spins, a)) return;
+    }
+}
+
+// the finisher of a level tries to advance the completed-level prefix
+__device__ __forceinline__ void advance_prefix(uint32_t l, const SweepArgs &a) {
+    while (true) {
+        if (ld_relaxed_u32(&a.st->prefix) != l - 1) return;
+        if (atomicCAS(&a.st->prefix, l - 1, l) != l - 1) return;
+        fence_sc();
+        ++l;
+        if (int(l) > a.nlev_total) return;
+        if (ld_relaxed_u32(a.lvl_cnt + l) != a.lvl_tiles[l]) return;
     }
 }
 
@@ -363,6 +403,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
     constexpr int BS2 = BS * BS;
     constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int last_cta;
     if (a.skip_flag && ld_relaxed_s32(a.skip_flag) != 0) return;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * a.stages;
@@ -396,74 +437,102 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         const int s = int(k % a.stages);
         const uint32_t ph = uint32_t(k / a.stages) & 1u;
         const bool up = t >= a.nl;
-        const int S = (up ? a.meta_u[t - a.nl] : a.meta_l[t]).nslot;
+        const TileMeta m = up ? a.meta_u[t - a.nl] : a.meta_l[t];
+        const int S = m.nslot;
+        const uint32_t lvl = uint32_t(up ? a.nlev_l + m.level : m.level);
         mbar_wait(bars + s, ph);
         const unsigned char *rec = stage0 + size_t(s) * a.stage_bytes;
-        if (lane < R) {
-            const int row = reinterpret_cast<const int *>(rec)[lane];
-            if (row >= 0) {
-                const int *cols = reinterpret_cast<const int *>(rec + 128);
-                const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
-                const double *dep = up ? a.x_t : a.y_t;
-                double acc[BS];
-                if (!up) {
+        const int row = lane < R ? reinterpret_cast<const int *>(rec)[lane] : -1;
+        double acc[BS];
+        if (row >= 0 && !up) {
 #pragma unroll
-                    for (int r = 0; r < BS; ++r) acc[r] = __ldg(a.b + int64_t(row) * BS + r);
-                } else {
-                    // own y_i (published by the L part of this same launch)
-                    int jj1[1] = {row};
-                    double yv[1][BS];
-                    wait_values<BS, 1>(a.y_t, jj1, yv, 1u, par, a);
-                    const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) {
-                        double z = 0.0;
-#pragma unroll
-                        for (int c = 0; c < BS; ++c) z = fma(dv[(c * BS + r) * R + lane], yv[0][c], z);
-                        acc[r] = z;
-                    }
-                }
-                for (int s0 = 0; s0 < S; s0 += CH) {
-                    int jj[CH];
-                    double xv[CH][BS];
-                    uint32_t pend = 0;
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        jj[c] = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
-                        if (jj[c] >= 0) pend |= 1u << c;
-                    }
-                    wait_values<BS, CH>(dep, jj, xv, pend, par, a);
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        if (jj[c] >= 0) {
-                            const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
-#pragma unroll
-                            for (int q = 0; q < BS; ++q)
-#pragma unroll
-                                for (int r = 0; r < BS; ++r) acc[r] = fma(-v[(q * BS + r) * R], xv[c][q], acc[r]);
-                        }
-                    }
-                }
-                double *dst = up ? a.x_t : a.y_t;
-#pragma unroll
-                for (int r = 0; r < BS; ++r) st_relaxed(dst + int64_t(row) * BS + r, tag(acc[r], par));
-                if (up && a.out) {
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];
-                }
+            for (int r = 0; r < BS; ++r) acc[r] = __ldg(a.b + int64_t(row) * BS + r);
+        }
+        // coarse wait: one lane, one load, back-off
+        if (lane == 0 && int(lvl) - a.gap > 0) {
+            uint64_t t0 = 0;
+            uint32_t spins = 0;
+            while (int(ld_relaxed_u32(&a.st->prefix)) < int(lvl) - a.gap) {
+                if (timed_out(t0, spins, a)) break;
+                if (a.coarse_sleep_ns) __nanosleep(a.coarse_sleep_ns);
             }
         }
         __syncwarp();
-        if (lane == 0 && t + int64_t(a.stages) * W < T) {
-            fence_proxy_async();
-            issue(t + int64_t(a.stages) * W, s);
+        if (row >= 0) {
+            const int *cols = reinterpret_cast<const int *>(rec + 128);
+            const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
+            const double *dep = up ? a.x_t : a.y_t;
+            if (up) {
+                // own y_i (published by the L part of this same launch)
+                int jj1[1] = {row};
+                double yv[1][BS];
+                wait_values<BS, 1>(a.y_t, jj1, yv, 1u, par, a);
+                const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
+#pragma unroll
+                for (int r = 0; r < BS; ++r) {
+                    double z = 0.0;
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) z = fma(dv[(c * BS + r) * R + lane], yv[0][c], z);
+                    acc[r] = z;
+                }
+            }
+            for (int s0 = 0; s0 < S; s0 += CH) {
+                int jj[CH];
+                double xv[CH][BS];
+                uint32_t pend = 0;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    jj[c] = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
+                    if (jj[c] >= 0) pend |= 1u << c;
+                }
+                wait_values<BS, CH>(dep, jj, xv, pend, par, a);
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    if (jj[c] >= 0) {
+                        const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
+#pragma unroll
+                        for (int q = 0; q < BS; ++q)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r) acc[r] = fma(-v[(q * BS + r) * R], xv[c][q], acc[r]);
+                    }
+                }
+            }
+            double *dst = up ? a.x_t : a.y_t;
+#pragma unroll
+            for (int r = 0; r < BS; ++r) st_relaxed(dst + int64_t(row) * BS + r, tag(acc[r], par));
+            if (up && a.out) {
+#pragma unroll
+                for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // progress accounting (hint): count the tile, advance the prefix on level completion
+            __threadfence();
+            if (atomicAdd(a.lvl_cnt + lvl, 1u) + 1 == a.lvl_tiles[lvl]) {
+                fence_sc();
+                advance_prefix(lvl, a);
+            }
+            if (t + int64_t(a.stages) * W < T) {
+                fence_proxy_async();
+                issue(t + int64_t(a.stages) * W, s);
+            }
         }
     }
     // the last CTA to finish advances the epoch (every CTA read it at entry)
+    // and resets the progress counters for the next launch
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&a.st->done_ctas, 1u) == gridDim.x - 1) {
+        last_cta = atomicAdd(&a.st->done_ctas, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_cta) {
+        __threadfence();
+        for (int l = threadIdx.x; l <= a.nlev_total + 1; l += blockDim.x) a.lvl_cnt[l] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            a.st->prefix = 0;
             a.st->done_ctas = 0;
             __threadfence();
             atomicAdd(&a.st->epoch, 1u);

@@ -22,7 +22,13 @@ struct SweepArgs {
     int stages;
     int stage_bytes;
     uint64_t timeout_ns;
-    int backoff_ns;
+    const uint32_t *lvl_tiles;   // tiles per combined level (1-based)
+    uint32_t *lvl_cnt;           // tiles finished per combined level (reset by the last CTA)
+    int nlev_l;                  // combined level of U' level l is nlev_l + l
+    int nlev_total;
+    int gap;
+    int coarse_sleep_ns;
+    int fine_sleep_ns;
 };
 
 cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);

@@ -155,6 +155,8 @@ void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int
             TileMeta m;
             m.off128 = uint32_t(sw.rec_total / 128);
             m.nslot = S;
+            m.level = l;
+            m.pad = 0;
             sw.meta.push_back(m);
             const int64_t bytes = rec_bytes(p.bs, S, upper);
             sw.rec_total += bytes;
@@ -242,6 +244,10 @@ int plan_analyse(Plan &p, int32_t bs, int64_t n, const int64_t *rp, const int64_
     }
     build_sweep(p, false, p.lev_L, p.nlev_L, p.sl);
     build_sweep(p, true, p.lev_U, p.nlev_U, p.su);
+    // tiles per combined level: L levels 1..nlev_L, then U' levels nlev_L+1..
+    p.lvl_tiles.assign(size_t(p.nlev_L) + p.nlev_U + 2, 0);
+    for (const TileMeta &m : p.sl.meta) p.lvl_tiles[m.level]++;
+    for (const TileMeta &m : p.su.meta) p.lvl_tiles[p.nlev_L + m.level]++;
     if ((p.sl.rec_total / 128) >= (int64_t(1) << 32) || (p.su.rec_total / 128) >= (int64_t(1) << 32))
         return fail(BILUK_EUNSUPPORTED, "factor records exceed 512 GB");
     return BILUK_OK;
@@ -286,6 +292,8 @@ int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, c
         for (int64_t i = t * R; i < std::min<int64_t>(n, (t + 1) * R); ++i) S = std::max(S, o.rp[i + 1] - o.rp[i]);
         o.meta[t].off128 = uint32_t(o.rec_total / 128);
         o.meta[t].nslot = S;
+        o.meta[t].level = 0;
+        o.meta[t].pad = 0;
         o.rec_total += ell_bytes(bs, S);
     }
     if (o.rec_total / 128 >= (int64_t(1) << 32)) return fail(BILUK_EUNSUPPORTED, "operator exceeds 512 GB");
@@ -297,7 +305,7 @@ int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, c
     };
     o.off.rp = take(4 * (n + 1));
     o.off.ci = take(4 * o.nnz);
-    o.off.meta = take(8 * o.ntiles);
+    o.off.meta = take(sizeof(TileMeta) * o.ntiles);
     o.off.rec = take(o.rec_total);
     o.off.total = off;
     return BILUK_OK;
@@ -336,13 +344,15 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.dinv = take(8 * p.n * bs2);
     const int R = rows_per_tile(p.bs);
     p.off.sl_rows = take(4 * p.sl.ntiles * R);
-    p.off.sl_meta = take(8 * p.sl.ntiles);
+    p.off.sl_meta = take(sizeof(TileMeta) * p.sl.ntiles);
     p.off.sl_rec = take(p.sl.rec_total);
     p.off.su_rows = take(4 * p.su.ntiles * R);
-    p.off.su_meta = take(8 * p.su.ntiles);
+    p.off.su_meta = take(sizeof(TileMeta) * p.su.ntiles);
     p.off.su_rec = take(p.su.rec_total);
     p.off.y_t = take(8 * p.n * p.bs);
     p.off.x_t = take(8 * p.n * p.bs);
+    p.off.lvl_tiles = take(4 * p.lvl_tiles.size());
+    p.off.lvl_cnt = take(4 * p.lvl_tiles.size());
     p.off.status = take(sizeof(DevStatus));
     p.off.total = o;
 }

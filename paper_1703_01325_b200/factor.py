@@ -98,6 +98,12 @@ class BlockIlukFactors:
         from .trisolve import apply_preconditioner
         return apply_preconditioner(self, b, out=out)
 
+    def tune(self, **knobs):
+        """Sweep-kernel knobs (gap, coarse_sleep_ns, fine_sleep_ns); results never depend on them."""
+        for key, val in knobs.items():
+            nat.check(nat.lib().biluk_plan_tune(self._h, key.encode(), int(val)))
+        return self
+
     def status(self):
         """Synchronise and raise if a device dependency wait timed out."""
         nat.check(nat.lib().biluk_plan_status(self._h, enter()), stage="apply")

@@ -55,6 +55,48 @@ def test_oracle_matches_reference_golden(path):
     assert abs(its - int(g["bicg_iters"])) <= 1 and conv == bool(g["bicg_conv"])
 
 
+@pytest.mark.parametrize("path", CASES, ids=[os.path.basename(p)[:-4] for p in CASES])
+def test_c_oracle_matches_reference_golden(path):
+    """The C restatement (oracle/coracle.c) used at full size is pinned the same way."""
+    from oracle import coracle
+    g = load_golden(path)
+    n, bs, k = int(g["n"]), int(g["bs"]), int(g["k"])
+    cf = coracle.CFactors(n, bs, g["rp"], g["ci"], g["vals"], k)
+    assert np.array_equal(cf.L_rp, g["L_rp"]) and np.array_equal(cf.L_ci, g["L_ci"])
+    assert np.array_equal(cf.U_rp, g["U_rp"]) and np.array_equal(cf.U_ci, g["U_ci"])
+    assert rel_err(cf.L_vals, g["L_vals"]) <= 1e-12
+    assert rel_err(cf.U_vals, g["U_vals"]) <= 1e-12
+    assert rel_err(cf.dinv, g["dinv"]) <= 1e-12
+    assert np.array_equal(cf.lo_level_of_row, g["lo_level_of_row"])
+    assert np.array_equal(cf.up_level_of_row, g["up_level_of_row"])
+    assert cf.plnnz == int(g["lo_nnz"]) and cf.punnz == int(g["up_nnz"])
+    assert rel_err(cf.apply(g["rhs"]), g["apply_out"]) <= 1e-12
+    from oracle import cbaseline
+    assert rel_err(cbaseline.PortApply(cf)(g["rhs"]), g["apply_out"]) <= 1e-12
+    ax = coracle.bsr_spmv(n, bs, g["rp"], g["ci"], g["vals"], np.ones(n * bs))
+    absax = coracle.bsr_spmv(n, bs, g["rp"], g["ci"], np.abs(g["vals"]), np.ones(n * bs))
+    assert np.abs(ax - g["spmv_ones"]).max() <= 1e-14 * absax.max()
+
+
+def test_c_oracle_errors():
+    from oracle import coracle
+    # singular leading 2x2 block (reference test_factor.py:145-155) -> code 2, row 0
+    rp = np.array([0, 2, 4], np.int64)
+    ci = np.array([0, 1, 0, 1], np.int64)
+    blk = np.zeros((4, 2, 2))
+    blk[0] = [[1.0, 2.0], [2.0, 4.0]]
+    blk[2] = np.eye(2)
+    blk[3] = np.eye(2)
+    vals = blk.transpose(0, 2, 1).reshape(-1)
+    with pytest.raises(coracle.COracleError) as exc:
+        coracle.CFactors(2, 2, rp, ci, vals, 0)
+    assert exc.value.code == 2 and exc.value.row == 0
+    # missing diagonal -> structural, row 0
+    with pytest.raises(coracle.COracleError) as exc:
+        coracle.CFactors(2, 1, np.array([0, 1, 2], np.int64), np.array([1, 0], np.int64), np.ones(2), 0)
+    assert exc.value.code == 1 and exc.value.row == 0
+
+
 def test_block_invert_known_answers():
     # reference test_factor.py:20-48
     inv = orc.block_invert(np.array([[1.0, 2.0], [3.0, 4.0]]))
