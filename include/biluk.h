@@ -116,6 +116,15 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
  *   "fine_sleep_ns"   back-off of the per-value dependency poll (default 0) */
 int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value);
 
+/* Diagnostics: when dev_trace != NULL every later apply writes, per tile
+ * (L tiles then U' tiles), 4 uint64 {record ready, released to poll, done,
+ * SM id} (globaltimer ns) into dev_trace.  NULL disables tracing. */
+int biluk_plan_set_trace(biluk_plan_t *plan, void *dev_trace);
+
+/* Combined dependency level of every tile (L tiles 1..levels_L, then U'
+ * tiles levels_L+1..), host array of info[9]+info[10] entries. */
+int biluk_plan_tile_levels(const biluk_plan_t *plan, int32_t *levels);
+
 /* Synchronises the stream and returns the sticky device status of the plan
  * (BILUK_OK or BILUK_ETIMEOUT), clearing it. */
 int biluk_plan_status(biluk_plan_t *plan, void *stream);

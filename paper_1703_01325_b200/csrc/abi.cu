@@ -229,7 +229,23 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.gap = p.tune.gap;
     a.coarse_sleep_ns = p.tune.coarse_sleep_ns;
     a.fine_sleep_ns = p.tune.fine_sleep_ns;
+    a.trace = p.trace;
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+    return BILUK_OK;
+}
+
+int biluk_plan_tile_levels(const biluk_plan_t *plan, int32_t *levels) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    const Plan &p = plan->p;
+    int64_t q = 0;
+    for (const TileMeta &m : p.sl.meta) levels[q++] = m.level;
+    for (const TileMeta &m : p.su.meta) levels[q++] = p.nlev_L + m.level;
+    return BILUK_OK;
+}
+
+int biluk_plan_set_trace(biluk_plan_t *plan, void *dev_trace) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    plan->p.trace = static_cast<unsigned long long *>(dev_trace);
     return BILUK_OK;
 }
 

@@ -108,6 +108,7 @@ struct Plan {
     Sweep sl, su;                    // L sweep, U' sweep
     std::vector<uint32_t> lvl_tiles; // tiles per combined level (L levels, then U' levels), 1-based
     SweepTune tune;
+    unsigned long long *trace = nullptr;   // optional per-tile timing records (diagnostics)
     // launch configuration of the sweep kernel
     int32_t sweep_ctas = 0, sweep_warps = 0, sweep_stages = 0;
     int64_t stage_bytes = 0;

@@ -404,7 +404,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
     constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int last_cta;
+    __shared__ uint32_t cta_prefix;
     if (a.skip_flag && ld_relaxed_s32(a.skip_flag) != 0) return;
+    if (threadIdx.x == 0) cta_prefix = 0;
+    __syncthreads();
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * a.stages;
     unsigned char *stage0 = smem + align128(int64_t(nw) * a.stages * 8) + size_t(warp) * a.stages * a.stage_bytes;
@@ -448,16 +451,27 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
 #pragma unroll
             for (int r = 0; r < BS; ++r) acc[r] = __ldg(a.b + int64_t(row) * BS + r);
         }
-        // coarse wait: one lane, one load, back-off
+        uint64_t tr0 = 0;
+        if (a.trace && lane == 0) tr0 = globaltimer();
+        // coarse wait: one lane per warp; the CTA shares the last prefix value
+        // it saw (shared memory) so the global word is read at most by a few
+        // warps, and the back-off grows with the distance to the target level
         if (lane == 0 && int(lvl) - a.gap > 0) {
+            const int target = int(lvl) - a.gap;
             uint64_t t0 = 0;
             uint32_t spins = 0;
-            while (int(ld_relaxed_u32(&a.st->prefix)) < int(lvl) - a.gap) {
+            while (int(*reinterpret_cast<volatile uint32_t *>(&cta_prefix)) < target) {
+                const int p = int(ld_relaxed_u32(&a.st->prefix));
+                atomicMax(&cta_prefix, uint32_t(p));
+                if (p >= target) break;
                 if (timed_out(t0, spins, a)) break;
-                if (a.coarse_sleep_ns) __nanosleep(a.coarse_sleep_ns);
+                const int d = target - p;
+                __nanosleep(uint32_t(min(a.coarse_sleep_ns * d, 4000)));
             }
         }
         __syncwarp();
+        uint64_t tr1 = 0;
+        if (a.trace && lane == 0) tr1 = globaltimer();
         if (row >= 0) {
             const int *cols = reinterpret_cast<const int *>(rec + 128);
             const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
@@ -507,8 +521,14 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         }
         __syncwarp();
         if (lane == 0) {
-            // progress accounting (hint): count the tile, advance the prefix on level completion
-            __threadfence();
+            if (a.trace) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                ulonglong4 rec4 = make_ulonglong4(tr0, tr1, globaltimer(), smid);
+                reinterpret_cast<ulonglong4 *>(a.trace)[t] = rec4;
+            }
+            // progress accounting (a hint only): count the tile, advance the
+            // completed-level prefix when this tile completes its level
             if (atomicAdd(a.lvl_cnt + lvl, 1u) + 1 == a.lvl_tiles[lvl]) {
                 fence_sc();
                 advance_prefix(lvl, a);

@@ -29,6 +29,7 @@ struct SweepArgs {
     int gap;
     int coarse_sleep_ns;
     int fine_sleep_ns;
+    unsigned long long *trace;   // optional: per tile {t_ready, t_released, t_done, smid}
 };
 
 cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);

@@ -104,6 +104,26 @@ class BlockIlukFactors:
             nat.check(nat.lib().biluk_plan_tune(self._h, key.encode(), int(val)))
         return self
 
+    def tile_levels(self):
+        """Combined dependency level of every sweep tile (L tiles, then U' tiles)."""
+        inf = self.info
+        out = np.zeros(inf["tiles_L"] + inf["tiles_U"], np.int32)
+        nat.check(nat.lib().biluk_plan_tile_levels(self._h, nat.ptr(out)))
+        return out
+
+    def set_trace(self, enable=True):
+        """Diagnostics: record per-tile globaltimer stamps on later applies; returns the (T, 4) buffer."""
+        if not enable:
+            nat.check(nat.lib().biluk_plan_set_trace(self._h, None))
+            self._trace = None
+            return None
+        from .device import torch
+        t = torch()
+        inf = self.info
+        self._trace = t.zeros((inf["tiles_L"] + inf["tiles_U"], 4), dtype=t.int64, device="cuda")
+        nat.check(nat.lib().biluk_plan_set_trace(self._h, self._trace.data_ptr()))
+        return self._trace
+
     def status(self):
         """Synchronise and raise if a device dependency wait timed out."""
         nat.check(nat.lib().biluk_plan_status(self._h, enter()), stage="apply")
