@@ -229,6 +229,7 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.gap = p.tune.gap;
     a.coarse_sleep_ns = p.tune.coarse_sleep_ns;
     a.fine_sleep_ns = p.tune.fine_sleep_ns;
+    a.poll_all = p.tune.poll_all;
     a.trace = p.trace;
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
     return BILUK_OK;
@@ -256,6 +257,8 @@ int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value) {
     if (k == "gap") t.gap = int(value);
     else if (k == "coarse_sleep_ns") t.coarse_sleep_ns = int(value);
     else if (k == "fine_sleep_ns") t.fine_sleep_ns = int(value);
+    else if (k == "warps") t.warps = int(value);
+    else if (k == "poll_all") t.poll_all = int(value);
     else return fail(BILUK_EARG, "unknown tuning key " + k);
     return BILUK_OK;
 }

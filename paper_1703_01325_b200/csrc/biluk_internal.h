@@ -77,9 +77,11 @@ struct DevStatus {
 
 // runtime knobs of the sweep (biluk_plan_tune)
 struct SweepTune {
-    int gap = 2;             // fine-grained polling starts once prefix >= level - gap
+    int gap = 2;             // fine-grained polling starts once prefix >= level - gap (<= 0: no gate, no counters)
     int coarse_sleep_ns = 64;
     int fine_sleep_ns = 0;
+    int warps = 0;           // warps per CTA actually launched (0 = the planned maximum)
+    int poll_all = 0;        // 1: poll every component at once (one round trip, more traffic)
 };
 
 struct Sweep {                       // host copy of one sweep's tile layout

@@ -352,7 +352,7 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ src, cons
     uint64_t t0 = 0;
     uint32_t spins = 0;
     // phase 1: poll the last component of every pending dependency
-    uint32_t todo = pend;
+    uint32_t todo = a.poll_all ? 0u : pend;
     while (todo) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
@@ -382,6 +382,7 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ src, cons
         }
         if (!pend) break;
         if (timed_out(t0, spins, a)) return;
+        if (a.poll_all && a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
     }
 }
 
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         // coarse wait: one lane per warp; the CTA shares the last prefix value
         // it saw (shared memory) so the global word is read at most by a few
         // warps, and the back-off grows with the distance to the target level
-        if (lane == 0 && int(lvl) - a.gap > 0) {
+        if (lane == 0 && a.gap > 0 && int(lvl) - a.gap > 0) {
             const int target = int(lvl) - a.gap;
             uint64_t t0 = 0;
             uint32_t spins = 0;
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
             }
             // progress accounting (a hint only): count the tile, advance the
             // completed-level prefix when this tile completes its level
-            if (atomicAdd(a.lvl_cnt + lvl, 1u) + 1 == a.lvl_tiles[lvl]) {
+            if (a.gap > 0 && atomicAdd(a.lvl_cnt + lvl, 1u) + 1 == a.lvl_tiles[lvl]) {
                 fence_sc();
                 advance_prefix(lvl, a);
             }
@@ -712,14 +713,18 @@ cudaError_t launch_pack_ell(const Op &o, const double *avals, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static int launch_warps(const Plan &p) {
+    return (p.tune.warps > 0 && p.tune.warps < p.sweep_warps) ? p.tune.warps : p.sweep_warps;
+}
+
 size_t sweep_smem_bytes(const Plan &p) {
-    return size_t(align128(int64_t(p.sweep_warps) * p.sweep_stages * 8)) +
-           size_t(p.sweep_warps) * p.sweep_stages * size_t(p.stage_bytes);
+    const int w = launch_warps(p);
+    return size_t(align128(int64_t(w) * p.sweep_stages * 8)) + size_t(w) * p.sweep_stages * size_t(p.stage_bytes);
 }
 
 cudaError_t launch_sweep(const Plan &p, const SweepArgs &a, cudaStream_t s) {
     const size_t smem = sweep_smem_bytes(p);
-    dim3 grid(p.sweep_ctas), block(p.sweep_warps * 32);
+    dim3 grid(p.sweep_ctas), block(launch_warps(p) * 32);
 #define SWEEP_LAUNCH(BS)                                                                                   \
     {                                                                                                      \
         auto kern = sweep_kernel<BS>;                                                                      \

@@ -29,6 +29,7 @@ struct SweepArgs {
     int gap;
     int coarse_sleep_ns;
     int fine_sleep_ns;
+    int poll_all;
     unsigned long long *trace;   // optional: per tile {t_ready, t_released, t_done, smid}
 };
 
