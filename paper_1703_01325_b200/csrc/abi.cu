@@ -34,6 +34,16 @@ static int cuda_fail(cudaError_t e, const char *what) {
 
 static DevStatus *dev_status(Plan &p) { return reinterpret_cast<DevStatus *>(p.ws + p.off.status); }
 
+static int64_t npos_l(const Plan &p) { return p.sl.ntiles * rows_per_tile(p.bs); }
+static int64_t npos_u(const Plan &p) { return p.su.ntiles * rows_per_tile(p.bs); }
+
+// the parity-tagged sweep vectors restart at parity 0 (so the next apply, parity 1, sees no stale data)
+static cudaError_t clear_tagged(Plan &p, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * npos_l(p) * p.bs, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * npos_u(p) * p.bs, s);
+    return e;
+}
+
 int64_t apply_bytes(const Plan &p) {
     // 8b^2(nL+nU+n) + 4(nL+nU) + 8(n+1) + 32bn
     const int64_t b = p.bs;
@@ -158,9 +168,10 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     CUDA_TRY(up(p.off.su_meta, p.su.meta.data(), sizeof(TileMeta) * p.su.meta.size()), "upload");
     CUDA_TRY(up(p.off.lvl_tiles, p.lvl_tiles.data(), 4 * p.lvl_tiles.size()), "upload");
     CUDA_TRY(cudaMemsetAsync(p.ws + p.off.lvl_cnt, 0, 4 * p.lvl_tiles.size(), s), "memset");
+    CUDA_TRY(up(p.off.pos_l, p.sl.pos.data(), 4 * p.sl.pos.size()), "upload");
+    CUDA_TRY(up(p.off.pos_u, p.su.pos.data(), 4 * p.su.pos.size()), "upload");
     // parity-tagged vectors start at parity 0 everywhere; the first apply uses parity 1
-    CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
-    CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
+    CUDA_TRY(clear_tagged(p, s), "memset");
     DevStatus init{};
     init.epoch = 1;
     init.ferr_row = (long long)INT64_MAX;
@@ -216,6 +227,8 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.b = dev_b;
     a.y_t = reinterpret_cast<double *>(p.ws + p.off.y_t);
     a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
+    a.npos_l = npos_l(p);
+    a.npos_u = npos_u(p);
     a.out = dev_x;
     a.st = dev_status(p);
     a.skip_flag = nullptr;
@@ -279,8 +292,7 @@ int biluk_plan_status(biluk_plan_t *plan, void *stream) {
         CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->done_ctas, &zero, 4, cudaMemcpyHostToDevice, s), "status reset");
         CUDA_TRY(cudaMemcpyAsync(&dev_status(p)->prefix, &zero, 4, cudaMemcpyHostToDevice, s), "status reset");
         CUDA_TRY(cudaMemsetAsync(p.ws + p.off.lvl_cnt, 0, 4 * p.lvl_tiles.size(), s), "memset");
-        CUDA_TRY(cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * p.n * p.bs, s), "memset");
-        CUDA_TRY(cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * p.n * p.bs, s), "memset");
+        CUDA_TRY(clear_tagged(p, s), "memset");
         CUDA_TRY(cudaStreamSynchronize(s), "status sync");
         return fail(code, "device dependency wait timed out in the triangular sweep");
     }

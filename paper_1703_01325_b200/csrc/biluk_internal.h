@@ -26,11 +26,16 @@ int fail(int code, const std::string &msg);
 // ---------------------------------------------------------------------------
 // tile geometry (shared by host planner and device kernels)
 //
-// A sweep processes block rows in level-major order, R rows per "tile"; one
-// warp owns one tile at a time, one lane per block row (lanes >= R idle).
+// A sweep processes block rows in level-major order (ascending row index
+// inside a level), R rows per "tile"; one warp owns one tile at a time, one
+// lane per block row (lanes >= R idle).  Row i of a sweep has a POSITION
+// pos = tile * R + lane; the sweep's intermediate vector lives at positions,
+// component-major (v[c * npos + pos]), so the 32 dependencies a warp reads
+// are (near-)contiguous and a published tile is one coalesced store.
 // A tile record is one contiguous, 128-byte aligned byte range:
-//   rows  int32[R]                       (128 B; -1 = padding row)
-//   cols  int32[S][R]                    (aligned up to 128 B; -1 = padding slot)
+//   rows  int32[R]                       (128 B; natural row index, -1 = padding)
+//   ypos  int32[R]                       (128 B; U' sweep only: the row's L position)
+//   cols  int32[S][R]                    (dependency POSITIONS; -1 = padding slot)
 //   dinv  f64[bs*bs][R]                  (U' sweep only: D^-1 of the row)
 //   vals  f64[S][bs*bs][R]               (block values, element e = c*bs + r)
 // so that a whole tile is moved by ONE bulk async copy (cp.async.bulk) and
@@ -40,13 +45,15 @@ BILUK_HD constexpr inline int rows_per_tile(int bs) {
     return bs <= 4 ? 32 : (bs <= 6 ? 16 : 8);
 }
 BILUK_HD constexpr inline int64_t align128(int64_t x) { return (x + 127) & ~int64_t(127); }
-BILUK_HD constexpr inline int64_t rec_cols_off() { return 128; }
+// header: rows int32[R] (natural block-row index, -1 = padding); U' tiles add
+// ypos int32[R] (the row's position in the L sweep, where its y lives)
+BILUK_HD constexpr inline int64_t rec_hdr_bytes(bool upper) { return upper ? 256 : 128; }
 BILUK_HD constexpr inline int64_t rec_cols_bytes(int bs, int S) {
     return align128(int64_t(S) * rows_per_tile(bs) * 4);
 }
-BILUK_HD constexpr inline int64_t rec_dinv_off(int bs, int S) { return 128 + rec_cols_bytes(bs, S); }
+BILUK_HD constexpr inline int64_t rec_dinv_off(int bs, int S) { return 256 + rec_cols_bytes(bs, S); }
 BILUK_HD constexpr inline int64_t rec_vals_off(int bs, int S, bool upper) {
-    return rec_dinv_off(bs, S) + (upper ? int64_t(bs) * bs * rows_per_tile(bs) * 8 : 0);
+    return upper ? rec_dinv_off(bs, S) + int64_t(bs) * bs * rows_per_tile(bs) * 8 : 128 + rec_cols_bytes(bs, S);
 }
 BILUK_HD constexpr inline int64_t rec_bytes(int bs, int S, bool upper) {
     return align128(rec_vals_off(bs, S, upper) + int64_t(S) * bs * bs * rows_per_tile(bs) * 8);
@@ -87,6 +94,7 @@ struct SweepTune {
 struct Sweep {                       // host copy of one sweep's tile layout
     int64_t ntiles = 0;
     std::vector<int32_t> tile_rows;  // ntiles * R
+    std::vector<int32_t> pos;        // n: position of every block row in this sweep
     std::vector<TileMeta> meta;      // ntiles
     int64_t rec_total = 0;           // bytes of all records
     int32_t max_slots = 0;
@@ -118,7 +126,7 @@ struct Plan {
     // workspace layout (byte offsets)
     struct {
         uint64_t p_rp, p_ci, p_diag, a2p, forder, pvals, dinv, sl_rows, sl_meta, sl_rec, su_rows, su_meta,
-            su_rec, y_t, x_t, lvl_tiles, lvl_cnt, status, total;
+            su_rec, pos_l, pos_u, y_t, x_t, lvl_tiles, lvl_cnt, status, total;
     } off{};
     // bound device pointers
     unsigned char *ws = nullptr;

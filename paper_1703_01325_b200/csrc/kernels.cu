@@ -247,7 +247,8 @@ template <int BS>
 __global__ void pack_sweep_kernel(int64_t ntiles, const TileMeta *__restrict__ meta, const int32_t *__restrict__ trows,
                                   unsigned char *__restrict__ rec, bool upper, const int32_t *__restrict__ rp,
                                   const int32_t *__restrict__ ci, const int32_t *__restrict__ diag,
-                                  const double *__restrict__ pvals, const double *__restrict__ dinv) {
+                                  const double *__restrict__ pvals, const double *__restrict__ dinv,
+                                  const int32_t *__restrict__ pos_dep, const int32_t *__restrict__ pos_l) {
     constexpr int R = rows_per_tile(BS);
     constexpr int BS2 = BS * BS;
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < ntiles * R; g += int64_t(gridDim.x) * blockDim.x) {
@@ -258,16 +259,17 @@ __global__ void pack_sweep_kernel(int64_t ntiles, const TileMeta *__restrict__ m
         unsigned char *r0 = rec + int64_t(m.off128) * 128;
         const int32_t row = trows[g];
         reinterpret_cast<int32_t *>(r0)[lane] = row;
+        if (upper) reinterpret_cast<int32_t *>(r0 + 128)[lane] = row >= 0 ? pos_l[row] : -1;
         int32_t base = 0, cnt = 0;
         if (row >= 0) {
             base = upper ? diag[row] + 1 : rp[row];
             cnt = upper ? rp[row + 1] - diag[row] - 1 : diag[row] - rp[row];
         }
-        int32_t *cols = reinterpret_cast<int32_t *>(r0 + 128);
+        int32_t *cols = reinterpret_cast<int32_t *>(r0 + rec_hdr_bytes(upper));
         double *vals = reinterpret_cast<double *>(r0 + rec_vals_off(BS, S, upper));
         for (int s = 0; s < S; ++s) {
             const bool live = s < cnt;
-            cols[s * R + lane] = live ? ci[base + s] : -1;
+            cols[s * R + lane] = live ? pos_dep[ci[base + s]] : -1;
             const double *src = pvals + int64_t(base + s) * BS2;
             for (int x = 0; x < BS2; ++x) vals[(int64_t(s) * BS2 + x) * R + lane] = live ? src[x] : 0.0;
         }
@@ -345,10 +347,11 @@ __device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const S
     return false;
 }
 
-// load the BS components of each pending dependency, values untagged
+// load the BS components of each pending dependency (positions jj in a
+// component-major vector of npos positions), values untagged
 template <int BS, int CH>
-__device__ __forceinline__ void wait_values(const double *__restrict__ src, const int (&jj)[CH], double (&xv)[CH][BS],
-                                            uint32_t pend, uint32_t par, const SweepArgs &a) {
+__device__ __forceinline__ void wait_values(const double *__restrict__ src, int64_t npos, const int (&jj)[CH],
+                                            double (&xv)[CH][BS], uint32_t pend, uint32_t par, const SweepArgs &a) {
     uint64_t t0 = 0;
     uint32_t spins = 0;
     // phase 1: poll the last component of every pending dependency
@@ -357,7 +360,7 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ src, cons
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             if (todo & (1u << c)) {
-                const double v = ld_relaxed(src + int64_t(jj[c]) * BS + (BS - 1));
+                const double v = ld_relaxed(src + (BS - 1) * npos + jj[c]);
                 if (tag_of(v) == par) todo &= ~(1u << c);
             }
         }
@@ -373,7 +376,7 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ src, cons
                 uint32_t ok = 1;
 #pragma unroll
                 for (int q = 0; q < BS; ++q) {
-                    const double v = ld_relaxed(src + int64_t(jj[c]) * BS + q);
+                    const double v = ld_relaxed(src + q * npos + jj[c]);
                     ok &= (tag_of(v) == par);
                     xv[c][q] = untag(v);
                 }
@@ -474,14 +477,15 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         uint64_t tr1 = 0;
         if (a.trace && lane == 0) tr1 = globaltimer();
         if (row >= 0) {
-            const int *cols = reinterpret_cast<const int *>(rec + 128);
+            const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
             const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
             const double *dep = up ? a.x_t : a.y_t;
+            const int64_t npos = up ? a.npos_u : a.npos_l;
             if (up) {
-                // own y_i (published by the L part of this same launch)
-                int jj1[1] = {row};
+                // own y_i (published by the L part of this same launch, at its L position)
+                int jj1[1] = {reinterpret_cast<const int *>(rec + 128)[lane]};
                 double yv[1][BS];
-                wait_values<BS, 1>(a.y_t, jj1, yv, 1u, par, a);
+                wait_values<BS, 1>(a.y_t, a.npos_l, jj1, yv, 1u, par, a);
                 const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
 #pragma unroll
                 for (int r = 0; r < BS; ++r) {
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                     jj[c] = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
                     if (jj[c] >= 0) pend |= 1u << c;
                 }
-                wait_values<BS, CH>(dep, jj, xv, pend, par, a);
+                wait_values<BS, CH>(dep, npos, jj, xv, pend, par, a);
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
                     if (jj[c] >= 0) {
@@ -512,9 +516,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                     }
                 }
             }
-            double *dst = up ? a.x_t : a.y_t;
+            // publish at this row's own position: one coalesced store per component
+            double *dst = (up ? a.x_t : a.y_t) + (up ? t - a.nl : t) * R + lane;
 #pragma unroll
-            for (int r = 0; r < BS; ++r) st_relaxed(dst + int64_t(row) * BS + r, tag(acc[r], par));
+            for (int r = 0; r < BS; ++r) st_relaxed(dst + r * npos, tag(acc[r], par));
             if (up && a.out) {
 #pragma unroll
                 for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];
@@ -683,16 +688,20 @@ cudaError_t launch_pack(const Plan &p, cudaStream_t s) {
     const int32_t *dg = reinterpret_cast<const int32_t *>(p.ws + p.off.p_diag);
     const double *pv = reinterpret_cast<const double *>(p.ws + p.off.pvals);
     const double *dv = reinterpret_cast<const double *>(p.ws + p.off.dinv);
+    const int32_t *pl = reinterpret_cast<const int32_t *>(p.ws + p.off.pos_l);
+    const int32_t *pu = reinterpret_cast<const int32_t *>(p.ws + p.off.pos_u);
 #define PACK_LAUNCH(BS)                                                                                        \
     {                                                                                                          \
         if (p.sl.ntiles)                                                                                       \
             pack_sweep_kernel<BS><<<grid_for(p.sl.ntiles * R, 128, p.num_sms), 128, 0, s>>>(                   \
                 p.sl.ntiles, reinterpret_cast<const TileMeta *>(p.ws + p.off.sl_meta),                         \
-                reinterpret_cast<const int32_t *>(p.ws + p.off.sl_rows), p.ws + p.off.sl_rec, false, rp, ci, dg, pv, dv); \
+                reinterpret_cast<const int32_t *>(p.ws + p.off.sl_rows), p.ws + p.off.sl_rec, false, rp, ci, dg, pv, dv, \
+                pl, pl);                                                                                       \
         if (p.su.ntiles)                                                                                       \
             pack_sweep_kernel<BS><<<grid_for(p.su.ntiles * R, 128, p.num_sms), 128, 0, s>>>(                   \
                 p.su.ntiles, reinterpret_cast<const TileMeta *>(p.ws + p.off.su_meta),                         \
-                reinterpret_cast<const int32_t *>(p.ws + p.off.su_rows), p.ws + p.off.su_rec, true, rp, ci, dg, pv, dv); \
+                reinterpret_cast<const int32_t *>(p.ws + p.off.su_rows), p.ws + p.off.su_rec, true, rp, ci, dg, pv, dv, \
+                pu, pl);                                                                                       \
     }
     BILUK_BS_DISPATCH(p.bs, PACK_LAUNCH)
 #undef PACK_LAUNCH

@@ -14,8 +14,9 @@ struct SweepArgs {
     const unsigned char *rec_u;
     int64_t nl, nu;          // tiles of the L and U' sweeps
     const double *b;         // right-hand side (n*bs)
-    double *y_t;             // parity-tagged intermediate y
-    double *x_t;             // parity-tagged result x (dependency copy)
+    double *y_t;             // parity-tagged intermediate y at L positions, component-major
+    double *x_t;             // parity-tagged result x at U' positions, component-major
+    int64_t npos_l, npos_u;  // positions (= tiles * R) of the two sweeps
     double *out;             // untagged result (may be null)
     DevStatus *st;
     const int *skip_flag;    // when non-null and *skip_flag != 0 the launch is a no-op

@@ -116,11 +116,12 @@ void level_schedule(int64_t m, const int64_t *rp, const int64_t *ci, bool upper,
 
 namespace {
 
-// Tiles of one sweep: rows grouped by block level; inside a level, rows with
-// more slots first (so a tile's rows have near-equal slot counts and padding
-// stays small), ties by ascending row.  Tiles never straddle two levels, so
-// every dependency of a tile lives in a strictly earlier tile -- the
-// deadlock-freedom argument of the persistent sweep.
+// Tiles of one sweep: rows grouped by block level, ascending row index inside
+// a level.  On stencil matrices the dependencies of consecutive rows of a
+// level are then consecutive rows of earlier levels, so a warp's dependency
+// loads coalesce.  Tiles never straddle two levels, so every dependency of a
+// tile lives in a strictly earlier tile -- the deadlock-freedom argument of
+// the persistent sweep.
 void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int32_t nlev, Sweep &sw) {
     const int R = rows_per_tile(p.bs);
     const int64_t n = p.n;
@@ -138,16 +139,17 @@ void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int
     }
     sw.tile_rows.clear();
     sw.meta.clear();
+    sw.pos.assign(n, -1);
     sw.rec_total = 0;
     sw.max_slots = 0;
     sw.max_rec = 0;
     for (int l = 1; l <= nlev; ++l) {
         auto b = order.begin() + start[l], e = order.begin() + start[l] + cnt[l];
-        std::stable_sort(b, e, [&](int32_t x, int32_t y) { return nslot(x) > nslot(y); });
         for (auto it = b; it < e; it += R) {
             const int64_t take = std::min<int64_t>(R, e - it);
             int32_t S = 0;
             for (int64_t q = 0; q < take; ++q) {
+                sw.pos[it[q]] = int32_t(sw.tile_rows.size());
                 sw.tile_rows.push_back(it[q]);
                 S = std::max(S, nslot(it[q]));
             }
@@ -349,8 +351,10 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.su_rows = take(4 * p.su.ntiles * R);
     p.off.su_meta = take(sizeof(TileMeta) * p.su.ntiles);
     p.off.su_rec = take(p.su.rec_total);
-    p.off.y_t = take(8 * p.n * p.bs);
-    p.off.x_t = take(8 * p.n * p.bs);
+    p.off.pos_l = take(4 * p.n);
+    p.off.pos_u = take(4 * p.n);
+    p.off.y_t = take(8 * p.sl.ntiles * R * p.bs);   // component-major at L positions
+    p.off.x_t = take(8 * p.su.ntiles * R * p.bs);   // component-major at U' positions
     p.off.lvl_tiles = take(4 * p.lvl_tiles.size());
     p.off.lvl_cnt = take(4 * p.lvl_tiles.size());
     p.off.status = take(sizeof(DevStatus));
