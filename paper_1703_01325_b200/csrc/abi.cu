@@ -243,6 +243,8 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.coarse_sleep_ns = p.tune.coarse_sleep_ns;
     a.fine_sleep_ns = p.tune.fine_sleep_ns;
     a.poll_all = p.tune.poll_all;
+    a.probe = p.tune.probe;
+    a.probe_sleep_ns = p.tune.probe_sleep_ns;
     a.trace = p.trace;
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
     return BILUK_OK;
@@ -272,6 +274,8 @@ int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value) {
     else if (k == "fine_sleep_ns") t.fine_sleep_ns = int(value);
     else if (k == "warps") t.warps = int(value);
     else if (k == "poll_all") t.poll_all = int(value);
+    else if (k == "probe") t.probe = int(value);
+    else if (k == "probe_sleep_ns") t.probe_sleep_ns = int(value);
     else return fail(BILUK_EARG, "unknown tuning key " + k);
     return BILUK_OK;
 }

@@ -68,7 +68,9 @@ struct TileMeta {      // 16 bytes
     uint32_t off128;   // record offset in 128-byte units
     int32_t nslot;     // S
     int32_t level;     // 1-based dependency level of the tile's rows (sweeps only)
-    int32_t pad;
+    int32_t probe;     // one dependency at level-1 to wait on cheaply before the full poll:
+                       // >= 0: position in this sweep's vector; <= -2: L position -(probe+2)
+                       // of a y value (U' tiles of level 1); -1: none
 };
 
 // device status block (lives in the workspace)
@@ -84,11 +86,13 @@ struct DevStatus {
 
 // runtime knobs of the sweep (biluk_plan_tune)
 struct SweepTune {
-    int gap = 2;             // fine-grained polling starts once prefix >= level - gap (<= 0: no gate, no counters)
+    int gap = 0;             // fine-grained polling starts once prefix >= level - gap (<= 0: no gate, no counters)
     int coarse_sleep_ns = 64;
     int fine_sleep_ns = 0;
-    int warps = 0;           // warps per CTA actually launched (0 = the planned maximum)
-    int poll_all = 0;        // 1: poll every component at once (one round trip, more traffic)
+    int warps = 4;           // warps per CTA actually launched (0 = the planned maximum)
+    int poll_all = 1;        // 1: poll every component at once (one round trip, more traffic)
+    int probe = 1;           // 1: one lane waits on the tile's probe dependency before the full poll
+    int probe_sleep_ns = 32;
 };
 
 struct Sweep {                       // host copy of one sweep's tile layout

@@ -473,6 +473,19 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                 __nanosleep(uint32_t(min(a.coarse_sleep_ns * d, 4000)));
             }
         }
+        // cheap wait: one lane polls ONE dependency of the previous level (one
+        // 8-byte load, back-off) so that warps far ahead of the frontier do
+        // not flood their SM's load pipeline with full-warp polls
+        if (lane == 0 && a.probe && m.probe != -1) {
+            const double *pv = m.probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * (up ? a.npos_u : a.npos_l) + m.probe
+                                            : a.y_t + (BS - 1) * a.npos_l + (-m.probe - 2);
+            uint64_t t0 = 0;
+            uint32_t spins = 0;
+            while (tag_of(ld_relaxed(pv)) != par) {
+                if (timed_out(t0, spins, a)) break;
+                if (a.probe_sleep_ns) __nanosleep(a.probe_sleep_ns);
+            }
+        }
         __syncwarp();
         uint64_t tr1 = 0;
         if (a.trace && lane == 0) tr1 = globaltimer();

@@ -31,6 +31,8 @@ struct SweepArgs {
     int coarse_sleep_ns;
     int fine_sleep_ns;
     int poll_all;
+    int probe;
+    int probe_sleep_ns;
     unsigned long long *trace;   // optional: per tile {t_ready, t_released, t_done, smid}
 };
 

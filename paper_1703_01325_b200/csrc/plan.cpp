@@ -122,12 +122,14 @@ namespace {
 // loads coalesce.  Tiles never straddle two levels, so every dependency of a
 // tile lives in a strictly earlier tile -- the deadlock-freedom argument of
 // the persistent sweep.
-void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int32_t nlev, Sweep &sw) {
+void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int32_t nlev, Sweep &sw,
+                 const Sweep *lower_sweep) {
     const int R = rows_per_tile(p.bs);
     const int64_t n = p.n;
     auto nslot = [&](int64_t i) -> int32_t {
         return upper ? p.p_rp[i + 1] - p.p_diag[i] - 1 : p.p_diag[i] - p.p_rp[i];
     };
+    auto first_slot = [&](int64_t i) -> int32_t { return upper ? p.p_diag[i] + 1 : p.p_rp[i]; };
     std::vector<int64_t> cnt(nlev + 2, 0);
     for (int64_t i = 0; i < n; ++i) cnt[lev[i]]++;
     std::vector<int64_t> start(nlev + 2, 0);
@@ -148,17 +150,25 @@ void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int
         for (auto it = b; it < e; it += R) {
             const int64_t take = std::min<int64_t>(R, e - it);
             int32_t S = 0;
+            // probe: a dependency on the previous level (positions of earlier levels are known)
+            int32_t probe = -1;
             for (int64_t q = 0; q < take; ++q) {
-                sw.pos[it[q]] = int32_t(sw.tile_rows.size());
-                sw.tile_rows.push_back(it[q]);
-                S = std::max(S, nslot(it[q]));
+                const int64_t i = it[q];
+                sw.pos[i] = int32_t(sw.tile_rows.size());
+                sw.tile_rows.push_back(int32_t(i));
+                S = std::max(S, nslot(i));
+                for (int32_t t = first_slot(i), e = first_slot(i) + nslot(i); t < e; ++t) {
+                    const int32_t j = p.p_ci[t];
+                    if (lev[j] == l - 1) probe = std::max(probe, sw.pos[j]);
+                }
+                if (upper && l == 1 && lower_sweep) probe = std::min(probe, -(lower_sweep->pos[i] + 2));
             }
             for (int64_t q = take; q < R; ++q) sw.tile_rows.push_back(-1);
             TileMeta m;
             m.off128 = uint32_t(sw.rec_total / 128);
             m.nslot = S;
             m.level = l;
-            m.pad = 0;
+            m.probe = probe;
             sw.meta.push_back(m);
             const int64_t bytes = rec_bytes(p.bs, S, upper);
             sw.rec_total += bytes;
@@ -244,8 +254,8 @@ int plan_analyse(Plan &p, int32_t bs, int64_t n, const int64_t *rp, const int64_
         for (int l = 1; l <= p.nlev_L; ++l) cur[l] = p.fptr[l - 1];
         for (int64_t i = 0; i < n; ++i) p.forder[cur[p.lev_L[i]]++] = int32_t(i);
     }
-    build_sweep(p, false, p.lev_L, p.nlev_L, p.sl);
-    build_sweep(p, true, p.lev_U, p.nlev_U, p.su);
+    build_sweep(p, false, p.lev_L, p.nlev_L, p.sl, nullptr);
+    build_sweep(p, true, p.lev_U, p.nlev_U, p.su, &p.sl);
     // tiles per combined level: L levels 1..nlev_L, then U' levels nlev_L+1..
     p.lvl_tiles.assign(size_t(p.nlev_L) + p.nlev_U + 2, 0);
     for (const TileMeta &m : p.sl.meta) p.lvl_tiles[m.level]++;
@@ -295,7 +305,7 @@ int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, c
         o.meta[t].off128 = uint32_t(o.rec_total / 128);
         o.meta[t].nslot = S;
         o.meta[t].level = 0;
-        o.meta[t].pad = 0;
+        o.meta[t].probe = -1;
         o.rec_total += ell_bytes(bs, S);
     }
     if (o.rec_total / 128 >= (int64_t(1) << 32)) return fail(BILUK_EUNSUPPORTED, "operator exceeds 512 GB");

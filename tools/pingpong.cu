@@ -1,0 +1,95 @@
+// Inter-SM flag ping-pong latency on the B200 (diagnostic microbenchmark).
+// Two single-warp CTAs pass a counter back and forth through global memory;
+// one hop = store by one SM -> observed by the poll of another SM.
+// Optional background CTAs spin on private addresses to emulate polling load.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pingpong tools/pingpong.cu && ./pingpong
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint64_t gt() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+template <int MODE>
+__device__ __forceinline__ unsigned long long ld(const unsigned long long *p) {
+    unsigned long long v;
+    if (MODE == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else if (MODE == 1) asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else if (MODE == 2) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("atom.relaxed.gpu.global.or.b64 %0, [%1], 0;" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+template <int MODE>
+__device__ __forceinline__ void st(unsigned long long *p, unsigned long long v) {
+    if (MODE == 2) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else if (MODE == 1) asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int MODE>
+__global__ void pingpong(unsigned long long *a, unsigned long long *b, int iters, unsigned long long *out,
+                         volatile int *stop, unsigned long long *bg) {
+    if (blockIdx.x >= 2) {   // background pollers
+        unsigned long long *p = bg + blockIdx.x * 64 + (threadIdx.x & 31) * 2;
+        while (*stop == 0) {
+            unsigned long long v = ld<0>(p);
+            if (v == 12345) st<0>(p + 1, v);
+        }
+        return;
+    }
+    if (threadIdx.x != 0) return;
+    uint64_t t0 = gt();
+    if (blockIdx.x == 0) {
+        for (int k = 1; k <= iters; ++k) {
+            st<MODE>(a, (unsigned long long)k);
+            while (ld<MODE>(b) != (unsigned long long)k) {
+            }
+        }
+        out[0] = gt() - t0;
+        *stop = 1;
+    } else {
+        for (int k = 1; k <= iters; ++k) {
+            while (ld<MODE>(a) != (unsigned long long)k) {
+            }
+            st<MODE>(b, (unsigned long long)k);
+        }
+    }
+}
+
+template <int MODE>
+void run(const char *name, int bg_ctas, int far) {
+    unsigned long long *buf, *out, *bgbuf;
+    int *stop;
+    cudaMalloc(&buf, 1 << 20);
+    cudaMalloc(&out, 64);
+    cudaMalloc(&stop, 4);
+    cudaMalloc(&bgbuf, size_t(1 << 20) * 8);
+    cudaMemset(buf, 0, 1 << 20);
+    cudaMemset(stop, 0, 4);
+    cudaMemset(bgbuf, 0, size_t(1 << 20) * 8);
+    const int iters = 2000;
+    unsigned long long *a = buf, *b = buf + (far ? 4096 : 16);
+    pingpong<MODE><<<2 + bg_ctas, 32 * (bg_ctas ? 8 : 1)>>>(a, b, iters, out, stop, bgbuf);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long ns = 0;
+    cudaMemcpy(&ns, out, 8, cudaMemcpyDeviceToHost);
+    printf("{\"variant\": \"%s\", \"bg_ctas\": %d, \"far\": %d, \"hop_ns\": %.1f, \"err\": \"%s\"}\n", name, bg_ctas, far,
+           double(ns) / (2.0 * iters), cudaGetErrorString(e));
+    cudaFree(buf);
+    cudaFree(out);
+    cudaFree(stop);
+    cudaFree(bgbuf);
+}
+
+int main() {
+    for (int bg : {0, 146}) {
+        run<0>("relaxed.gpu", bg, 1);
+        run<1>("volatile", bg, 1);
+        run<2>("acquire/release", bg, 1);
+        run<3>("atom.or poll", bg, 1);
+    }
+    run<0>("relaxed.gpu same-line", 0, 0);
+    return 0;
+}
