@@ -34,13 +34,10 @@ static int cuda_fail(cudaError_t e, const char *what) {
 
 static DevStatus *dev_status(Plan &p) { return reinterpret_cast<DevStatus *>(p.ws + p.off.status); }
 
-static int64_t npos_l(const Plan &p) { return p.sl.ntiles * rows_per_tile(p.bs); }
-static int64_t npos_u(const Plan &p) { return p.su.ntiles * rows_per_tile(p.bs); }
-
 // the parity-tagged sweep vectors restart at parity 0 (so the next apply, parity 1, sees no stale data)
 static cudaError_t clear_tagged(Plan &p, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * npos_l(p) * p.bs, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * npos_u(p) * p.bs, s);
+    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * plan_npos(p) * p.bs, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * plan_npos(p) * p.bs, s);
     return e;
 }
 
@@ -227,8 +224,7 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.b = dev_b;
     a.y_t = reinterpret_cast<double *>(p.ws + p.off.y_t);
     a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
-    a.npos_l = npos_l(p);
-    a.npos_u = npos_u(p);
+    a.npos = plan_npos(p);
     a.out = dev_x;
     a.st = dev_status(p);
     a.skip_flag = nullptr;

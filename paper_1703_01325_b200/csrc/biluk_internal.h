@@ -154,6 +154,12 @@ struct Op {
     bool bound = false, valued = false;
 };
 
+// component stride of the position-indexed sweep vectors y_t / x_t
+inline int64_t plan_npos(const Plan &p) {
+    const int64_t a = p.sl.ntiles * rows_per_tile(p.bs), b = p.su.ntiles * rows_per_tile(p.bs);
+    return a > b ? a : b;
+}
+
 // host planner (plan.cpp)
 int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,
                    std::vector<int32_t> &out_ci, int64_t *err_row);

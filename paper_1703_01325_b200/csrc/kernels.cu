@@ -347,46 +347,40 @@ __device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const S
     return false;
 }
 
-// load the BS components of each pending dependency (positions jj in a
-// component-major vector of npos positions), values untagged
-template <int BS, int CH>
-__device__ __forceinline__ void wait_values(const double *__restrict__ src, int64_t npos, const int (&jj)[CH],
-                                            double (&xv)[CH][BS], uint32_t pend, uint32_t par, const SweepArgs &a) {
+// Wait for NE published values: entry e has its BS components at
+// p[e] + q * stride.  Every poll round issues ALL pending loads before
+// looking at any of them, so one round costs one L2 round trip however many
+// dependencies a row has (checking each value right after its own load would
+// serialise one round trip per dependency).  Values come back untagged.
+template <int BS, int NE>
+__device__ __forceinline__ void wait_values(const double *const (&p)[NE], int64_t stride, double (&xv)[NE][BS],
+                                            uint32_t pend, uint32_t par, const SweepArgs &a) {
     uint64_t t0 = 0;
     uint32_t spins = 0;
-    // phase 1: poll the last component of every pending dependency
-    uint32_t todo = a.poll_all ? 0u : pend;
-    while (todo) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            if (todo & (1u << c)) {
-                const double v = ld_relaxed(src + (BS - 1) * npos + jj[c]);
-                if (tag_of(v) == par) todo &= ~(1u << c);
-            }
-        }
-        if (!todo) break;
-        if (timed_out(t0, spins, a)) return;
-        if (a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
-    }
-    // phase 2: all components (already published in practice; re-poll if not)
     while (pend) {
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            if (pend & (1u << c)) {
-                uint32_t ok = 1;
+        for (int e = 0; e < NE; ++e)
+            if (pend & (1u << e)) {
 #pragma unroll
-                for (int q = 0; q < BS; ++q) {
-                    const double v = ld_relaxed(src + q * npos + jj[c]);
-                    ok &= (tag_of(v) == par);
-                    xv[c][q] = untag(v);
-                }
-                if (ok) pend &= ~(1u << c);
+                for (int q = 0; q < BS; ++q) xv[e][q] = ld_relaxed(p[e] + q * stride);
             }
+        uint32_t still = 0;
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            uint32_t ok = 1;
+#pragma unroll
+            for (int q = 0; q < BS; ++q) ok &= (tag_of(xv[e][q]) == par);
+            if (!ok) still |= 1u << e;
         }
+        pend &= still;
         if (!pend) break;
-        if (timed_out(t0, spins, a)) return;
-        if (a.poll_all && a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
+        if (timed_out(t0, spins, a)) break;
+        if (a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
     }
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) xv[e][q] = untag(xv[e][q]);
 }
 
 // the finisher of a level tries to advance the completed-level prefix
@@ -477,8 +471,8 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         // 8-byte load, back-off) so that warps far ahead of the frontier do
         // not flood their SM's load pipeline with full-warp polls
         if (lane == 0 && a.probe && m.probe != -1) {
-            const double *pv = m.probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * (up ? a.npos_u : a.npos_l) + m.probe
-                                            : a.y_t + (BS - 1) * a.npos_l + (-m.probe - 2);
+            const double *pv = m.probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * a.npos + m.probe
+                                            : a.y_t + (BS - 1) * a.npos + (-m.probe - 2);
             uint64_t t0 = 0;
             uint32_t spins = 0;
             while (tag_of(ld_relaxed(pv)) != par) {
@@ -493,34 +487,35 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
             const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
             const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
             const double *dep = up ? a.x_t : a.y_t;
-            const int64_t npos = up ? a.npos_u : a.npos_l;
-            if (up) {
-                // own y_i (published by the L part of this same launch, at its L position)
-                int jj1[1] = {reinterpret_cast<const int *>(rec + 128)[lane]};
-                double yv[1][BS];
-                wait_values<BS, 1>(a.y_t, a.npos_l, jj1, yv, 1u, par, a);
-                const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
-#pragma unroll
-                for (int r = 0; r < BS; ++r) {
-                    double z = 0.0;
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) z = fma(dv[(c * BS + r) * R + lane], yv[0][c], z);
-                    acc[r] = z;
-                }
-            }
-            for (int s0 = 0; s0 < S; s0 += CH) {
-                int jj[CH];
-                double xv[CH][BS];
+            const int64_t npos = a.npos;
+            for (int s0 = 0; s0 < S || (up && s0 == 0); s0 += CH) {
+                // entries 0..CH-1: dependencies of this chunk; entry CH: the
+                // row's own y_i (U' tiles, first chunk), polled in the same round
+                const double *pp[CH + 1];
+                double xv[CH + 1][BS];
                 uint32_t pend = 0;
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
-                    jj[c] = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
-                    if (jj[c] >= 0) pend |= 1u << c;
+                    const int j = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
+                    pp[c] = dep + (j >= 0 ? j : 0);
+                    if (j >= 0) pend |= 1u << c;
                 }
-                wait_values<BS, CH>(dep, npos, jj, xv, pend, par, a);
+                pp[CH] = a.y_t + (up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0);
+                if (up && s0 == 0) pend |= 1u << CH;
+                wait_values<BS, CH + 1>(pp, npos, xv, pend, par, a);
+                if (up && s0 == 0) {
+                    const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) {
+                        double z = 0.0;
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) z = fma(dv[(c * BS + r) * R + lane], xv[CH][c], z);
+                        acc[r] = z;
+                    }
+                }
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
-                    if (jj[c] >= 0) {
+                    if (s0 + c < S && cols[(s0 + c) * R + lane] >= 0) {
                         const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
 #pragma unroll
                         for (int q = 0; q < BS; ++q)

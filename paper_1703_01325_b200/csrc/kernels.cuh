@@ -16,7 +16,7 @@ struct SweepArgs {
     const double *b;         // right-hand side (n*bs)
     double *y_t;             // parity-tagged intermediate y at L positions, component-major
     double *x_t;             // parity-tagged result x at U' positions, component-major
-    int64_t npos_l, npos_u;  // positions (= tiles * R) of the two sweeps
+    int64_t npos;            // component stride of y_t / x_t (>= tiles * R of either sweep)
     double *out;             // untagged result (may be null)
     DevStatus *st;
     const int *skip_flag;    // when non-null and *skip_flag != 0 the launch is a no-op
