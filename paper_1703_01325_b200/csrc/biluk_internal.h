@@ -64,13 +64,14 @@ BILUK_HD constexpr inline int64_t ell_bytes(int bs, int S) {
     return align128(ell_vals_off(bs, S) + int64_t(S) * bs * bs * rows_per_tile(bs) * 8);
 }
 
-struct TileMeta {      // 16 bytes
+struct TileMeta {      // 32 bytes
     uint32_t off128;   // record offset in 128-byte units
     int32_t nslot;     // S
     int32_t level;     // 1-based dependency level of the tile's rows (sweeps only)
-    int32_t probe;     // one dependency at level-1 to wait on cheaply before the full poll:
-                       // >= 0: position in this sweep's vector; <= -2: L position -(probe+2)
-                       // of a y value (U' tiles of level 1); -1: none
+    int32_t probe[2];  // probe[d-1]: one ancestor at level - d to wait on cheaply before the
+                       // full poll: >= 0: position in this sweep's vector; <= -2: L position
+                       // -(probe+2) of a y value (U' tiles of the first levels); -1: none
+    int32_t pad[3];
 };
 
 // device status block (lives in the workspace)

@@ -470,9 +470,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         // cheap wait: one lane polls ONE dependency of the previous level (one
         // 8-byte load, back-off) so that warps far ahead of the frontier do
         // not flood their SM's load pipeline with full-warp polls
-        if (lane == 0 && a.probe && m.probe != -1) {
-            const double *pv = m.probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * a.npos + m.probe
-                                            : a.y_t + (BS - 1) * a.npos + (-m.probe - 2);
+        const int probe = (a.probe == 1 || a.probe == 2) ? m.probe[a.probe - 1] : -1;
+        if (lane == 0 && probe != -1) {
+            const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * a.npos + probe
+                                          : a.y_t + (BS - 1) * a.npos + (-probe - 2);
             uint64_t t0 = 0;
             uint32_t spins = 0;
             while (tag_of(ld_relaxed(pv)) != par) {

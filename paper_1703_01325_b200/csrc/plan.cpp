@@ -150,25 +150,35 @@ void build_sweep(const Plan &p, bool upper, const std::vector<int32_t> &lev, int
         for (auto it = b; it < e; it += R) {
             const int64_t take = std::min<int64_t>(R, e - it);
             int32_t S = 0;
-            // probe: a dependency on the previous level (positions of earlier levels are known)
-            int32_t probe = -1;
+            // probes: an ancestor one and two levels back (positions of earlier levels are known);
+            // U' tiles without such an ancestor wait on a y value of the L sweep instead
+            int32_t probe1 = -1, probe2 = -1, ypos = -1;
             for (int64_t q = 0; q < take; ++q) {
                 const int64_t i = it[q];
                 sw.pos[i] = int32_t(sw.tile_rows.size());
                 sw.tile_rows.push_back(int32_t(i));
                 S = std::max(S, nslot(i));
+                if (lower_sweep) ypos = std::max(ypos, lower_sweep->pos[i]);
                 for (int32_t t = first_slot(i), e = first_slot(i) + nslot(i); t < e; ++t) {
                     const int32_t j = p.p_ci[t];
-                    if (lev[j] == l - 1) probe = std::max(probe, sw.pos[j]);
+                    if (lev[j] != l - 1) continue;
+                    probe1 = std::max(probe1, sw.pos[j]);
+                    if (lower_sweep) ypos = std::max(ypos, lower_sweep->pos[j]);
+                    for (int32_t u = first_slot(j), f = first_slot(j) + nslot(j); u < f; ++u)
+                        if (lev[p.p_ci[u]] == l - 2) probe2 = std::max(probe2, sw.pos[p.p_ci[u]]);
                 }
-                if (upper && l == 1 && lower_sweep) probe = std::min(probe, -(lower_sweep->pos[i] + 2));
+            }
+            if (upper && ypos >= 0) {
+                if (probe1 < 0) probe1 = -(ypos + 2);
+                if (probe2 < 0) probe2 = -(ypos + 2);
             }
             for (int64_t q = take; q < R; ++q) sw.tile_rows.push_back(-1);
-            TileMeta m;
+            TileMeta m{};
             m.off128 = uint32_t(sw.rec_total / 128);
             m.nslot = S;
             m.level = l;
-            m.probe = probe;
+            m.probe[0] = probe1;
+            m.probe[1] = probe2;
             sw.meta.push_back(m);
             const int64_t bytes = rec_bytes(p.bs, S, upper);
             sw.rec_total += bytes;
@@ -302,10 +312,10 @@ int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, c
     for (int64_t t = 0; t < o.ntiles; ++t) {
         int32_t S = 0;
         for (int64_t i = t * R; i < std::min<int64_t>(n, (t + 1) * R); ++i) S = std::max(S, o.rp[i + 1] - o.rp[i]);
+        o.meta[t] = TileMeta{};
         o.meta[t].off128 = uint32_t(o.rec_total / 128);
         o.meta[t].nslot = S;
-        o.meta[t].level = 0;
-        o.meta[t].probe = -1;
+        o.meta[t].probe[0] = o.meta[t].probe[1] = -1;
         o.rec_total += ell_bytes(bs, S);
     }
     if (o.rec_total / 128 >= (int64_t(1) << 32)) return fail(BILUK_EUNSUPPORTED, "operator exceeds 512 GB");
