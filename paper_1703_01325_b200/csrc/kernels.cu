@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
             }
         }
         __syncwarp();
-        uint64_t tr1 = 0;
+        uint64_t tr1 = 0, tr_deps = 0;
         if (a.trace && lane == 0) tr1 = globaltimer();
         if (row >= 0) {
             const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                 pp[CH] = a.y_t + (up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0);
                 if (up && s0 == 0) pend |= 1u << CH;
                 wait_values<BS, CH + 1>(pp, npos, xv, pend, par, a);
+                if (a.trace && lane == 0 && s0 == 0) tr_deps = globaltimer();
                 if (up && s0 == 0) {
                     const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
 #pragma unroll
@@ -537,9 +538,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         __syncwarp();
         if (lane == 0) {
             if (a.trace) {
-                uint32_t smid;
-                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                ulonglong4 rec4 = make_ulonglong4(tr0, tr1, globaltimer(), smid);
+                ulonglong4 rec4 = make_ulonglong4(tr0, tr1, globaltimer(), tr_deps);
                 reinterpret_cast<ulonglong4 *>(a.trace)[t] = rec4;
             }
             // progress accounting (a hint only): count the tile, advance the

@@ -58,6 +58,67 @@ __global__ void pingpong(unsigned long long *a, unsigned long long *b, int iters
     }
 }
 
+// sweep-like hop: a full warp polls NL loads per lane (component-major
+// positions, like y_t), all lanes must see the token before publishing 3
+// tagged doubles per lane; the partner warp does the same on other addresses.
+template <int NL>
+__global__ void warp_pingpong(double *va, double *vb, int64_t npos, int iters, unsigned long long *out) {
+    if (blockIdx.x >= 2) return;
+    const int lane = threadIdx.x;
+    uint64_t t0 = gt();
+    double *mine = blockIdx.x == 0 ? va : vb;
+    double *other = blockIdx.x == 0 ? vb : va;
+    for (int k = 1; k <= iters; ++k) {
+        if (blockIdx.x == 0 || k > 0) {
+            if (blockIdx.x == 0) {
+                for (int c = 0; c < 3; ++c) {
+                    double v = double(k);
+                    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(mine + c * npos + lane), "d"(v) : "memory");
+                }
+            }
+            // poll: NL loads per lane, the first 3 are the partner's components
+            while (true) {
+                double x[NL];
+#pragma unroll
+                for (int q = 0; q < NL; ++q) {
+                    const double *p = other + (q % 3) * npos + lane + (q / 3) * 64;
+                    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(x[q]) : "l"(p) : "memory");
+                }
+                bool ok = true;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) ok &= (x[q] == double(k));
+                if (__all_sync(0xffffffffu, ok)) break;
+            }
+            if (blockIdx.x == 1) {
+                for (int c = 0; c < 3; ++c) {
+                    double v = double(k);
+                    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(mine + c * npos + lane), "d"(v) : "memory");
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && lane == 0) out[0] = gt() - t0;
+}
+
+template <int NL>
+void run_warp(const char *name) {
+    double *buf;
+    unsigned long long *out;
+    const int64_t npos = 1 << 16;
+    cudaMalloc(&buf, sizeof(double) * npos * 8);
+    cudaMalloc(&out, 64);
+    cudaMemset(buf, 0, sizeof(double) * npos * 8);
+    const int iters = 2000;
+    warp_pingpong<NL><<<2, 32>>>(buf, buf + npos * 4, npos, iters, out);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long ns = 0;
+    cudaMemcpy(&ns, out, 8, cudaMemcpyDeviceToHost);
+    printf("{\"variant\": \"%s\", \"hop_ns\": %.1f, \"err\": \"%s\"}\n", name, double(ns) / (2.0 * iters),
+           cudaGetErrorString(e));
+    cudaFree(buf);
+    cudaFree(out);
+}
+
 template <int MODE>
 void run(const char *name, int bg_ctas, int far) {
     unsigned long long *buf, *out, *bgbuf;
@@ -91,5 +152,8 @@ int main() {
         run<3>("atom.or poll", bg, 1);
     }
     run<0>("relaxed.gpu same-line", 0, 0);
+    run_warp<3>("warp 32 lanes x 3 loads (one dep, 3 components)");
+    run_warp<9>("warp 32 lanes x 9 loads (3 deps)");
+    run_warp<21>("warp 32 lanes x 21 loads (7 deps)");
     return 0;
 }
