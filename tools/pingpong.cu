@@ -100,6 +100,18 @@ __global__ void warp_pingpong(double *va, double *vb, int64_t npos, int iters, u
     if (blockIdx.x == 0 && lane == 0) out[0] = gt() - t0;
 }
 
+__global__ void timer_cost(unsigned long long *out) {
+    long long c0 = clock64();
+    uint64_t acc = 0;
+    for (int i = 0; i < 1000; ++i) acc += gt();
+    long long c1 = clock64();
+    for (int i = 0; i < 1000; ++i) acc += (uint64_t)clock64();
+    long long c2 = clock64();
+    out[0] = c1 - c0;
+    out[1] = c2 - c1;
+    out[2] = acc;
+}
+
 template <int NL>
 void run_warp(const char *name) {
     double *buf;
@@ -145,6 +157,15 @@ void run(const char *name, int bg_ctas, int far) {
 }
 
 int main() {
+    {
+        unsigned long long *o, h[3];
+        cudaMalloc(&o, 64);
+        timer_cost<<<1, 1>>>(o);
+        cudaMemcpy(h, o, 24, cudaMemcpyDeviceToHost);
+        printf("{\"globaltimer_cycles_per_read\": %.1f, \"clock64_cycles_per_read\": %.1f}\n", h[0] / 1000.0,
+               h[1] / 1000.0);
+        cudaFree(o);
+    }
     for (int bg : {0, 146}) {
         run<0>("relaxed.gpu", bg, 1);
         run<1>("volatile", bg, 1);
