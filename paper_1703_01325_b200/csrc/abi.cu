@@ -242,6 +242,7 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.probe = p.tune.probe;
     a.probe_sleep_ns = p.tune.probe_sleep_ns;
     a.trace = p.trace;
+    a.trace_mode = p.tune.trace_mode;
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
     return BILUK_OK;
 }
@@ -272,6 +273,7 @@ int biluk_plan_tune(biluk_plan_t *plan, const char *key, int64_t value) {
     else if (k == "poll_all") t.poll_all = int(value);
     else if (k == "probe") t.probe = int(value);
     else if (k == "probe_sleep_ns") t.probe_sleep_ns = int(value);
+    else if (k == "trace_mode") t.trace_mode = int(value);
     else return fail(BILUK_EARG, "unknown tuning key " + k);
     return BILUK_OK;
 }

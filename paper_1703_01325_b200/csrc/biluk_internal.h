@@ -92,8 +92,9 @@ struct SweepTune {
     int fine_sleep_ns = 0;
     int warps = 4;           // warps per CTA actually launched (0 = the planned maximum)
     int poll_all = 1;        // 1: poll every component at once (one round trip, more traffic)
-    int probe = 1;           // 1: one lane waits on the tile's probe dependency before the full poll
+    int probe = 0;           // d = 1, 2: one lane waits on an ancestor d levels back before the full poll
     int probe_sleep_ns = 32;
+    int trace_mode = 1;      // diagnostics layout of the per-tile trace
 };
 
 struct Sweep {                       // host copy of one sweep's tile layout

@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
         }
         __syncwarp();
         uint64_t tr1 = 0, tr_deps = 0;
+        long long cyc_deps = 0, cyc_fma = 0, cyc_st = 0;
         if (a.trace && lane == 0) tr1 = globaltimer();
         if (row >= 0) {
             const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
@@ -506,7 +507,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                 pp[CH] = a.y_t + (up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0);
                 if (up && s0 == 0) pend |= 1u << CH;
                 wait_values<BS, CH + 1>(pp, npos, xv, pend, par, a);
-                if (a.trace && lane == 0 && s0 == 0) tr_deps = globaltimer();
+                if (a.trace && lane == 0 && s0 == 0) {
+                    tr_deps = globaltimer();
+                    cyc_deps = clock64();
+                }
                 if (up && s0 == 0) {
                     const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
 #pragma unroll
@@ -528,6 +532,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                     }
                 }
             }
+            if (a.trace && lane == 0) cyc_fma = clock64() + 0 * acc[0];
             // publish at this row's own position: one coalesced store per component
             double *dst = (up ? a.x_t : a.y_t) + (up ? t - a.nl : t) * R + lane;
 #pragma unroll
@@ -536,11 +541,16 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
 #pragma unroll
                 for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];
             }
+            if (a.trace && lane == 0) cyc_st = clock64();
         }
         __syncwarp();
         if (lane == 0) {
             if (a.trace) {
-                ulonglong4 rec4 = make_ulonglong4(tr0, tr1, globaltimer(), tr_deps);
+                const long long cyc_done = clock64();
+                const unsigned long long packed =
+                    (unsigned long long)(cyc_fma - cyc_deps) | ((unsigned long long)(cyc_st - cyc_deps) << 21) |
+                    ((unsigned long long)(cyc_done - cyc_deps) << 42);
+                ulonglong4 rec4 = make_ulonglong4(tr0, tr1, globaltimer(), a.trace_mode == 2 ? packed : tr_deps);
                 reinterpret_cast<ulonglong4 *>(a.trace)[t] = rec4;
             }
             // progress accounting (a hint only): count the tile, advance the

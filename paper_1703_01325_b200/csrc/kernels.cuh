@@ -33,7 +33,8 @@ struct SweepArgs {
     int poll_all;
     int probe;
     int probe_sleep_ns;
-    unsigned long long *trace;   // optional: per tile {t_ready, t_released, t_done, smid}
+    unsigned long long *trace;   // optional: per tile {t_ready, t_released, t_done, t_deps | cycle splits}
+    int trace_mode;              // 1: t_deps in the 4th word; 2: packed cycle splits after the poll
 };
 
 cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);
