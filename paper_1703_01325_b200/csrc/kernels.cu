@@ -359,6 +359,10 @@ __device__ __forceinline__ void wait_values(const double *const (&p)[NE], int64_
                                             uint32_t pend, uint32_t par, const SweepArgs &a) {
     uint64_t t0 = 0;
     uint32_t spins = 0;
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) xv[e][q] = 0.0;   // entries never polled contribute zero
     while (pend) {
 #pragma unroll
         for (int e = 0; e < NE; ++e)
@@ -521,14 +525,22 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
                         acc[r] = z;
                     }
                 }
+                // products: warp-uniform slot loop (S is per tile), padding slots hold
+                // zero blocks and zero x, so no per-lane guards; each slot is an
+                // independent short FMA chain, summed into acc in slot order
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
-                    if (s0 + c < S && cols[(s0 + c) * R + lane] >= 0) {
+                    if (s0 + c < S) {
                         const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
+                        double pr[BS];
 #pragma unroll
-                        for (int q = 0; q < BS; ++q)
+                        for (int r = 0; r < BS; ++r) pr[r] = v[r * R] * xv[c][0];
 #pragma unroll
-                            for (int r = 0; r < BS; ++r) acc[r] = fma(-v[(q * BS + r) * R], xv[c][q], acc[r]);
+                        for (int q = 1; q < BS; ++q)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r) pr[r] = fma(v[(q * BS + r) * R], xv[c][q], pr[r]);
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) acc[r] -= pr[r];
                     }
                 }
             }

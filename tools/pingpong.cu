@@ -100,6 +100,30 @@ __global__ void warp_pingpong(double *va, double *vb, int64_t npos, int iters, u
     if (blockIdx.x == 0 && lane == 0) out[0] = gt() - t0;
 }
 
+__global__ void dfma_latency(double *io, unsigned long long *out) {
+    __shared__ double sm[256];
+    sm[threadIdx.x] = io[threadIdx.x];
+    __syncthreads();
+    double a = io[0], b = io[1], c = io[2];
+    long long c0 = clock64();
+    for (int i = 0; i < 1000; ++i) a = fma(a, b, c);   // dependent chain
+    long long c1 = clock64();
+    double s = 0.0;
+    int idx = threadIdx.x;
+    for (int i = 0; i < 1000; ++i) {                     // dependent LDS chain
+        s += sm[idx];
+        idx = (idx + int(sm[idx] != 12345.0)) & 255;
+    }
+    long long c2 = clock64();
+    float f = float(b), g = float(c), h = float(a);
+    for (int i = 0; i < 1000; ++i) h = fmaf(h, f, g);
+    long long c3 = clock64();
+    io[8] = a + s + h;
+    out[0] = c1 - c0;
+    out[1] = c2 - c1;
+    out[2] = c3 - c2;
+}
+
 __global__ void timer_cost(unsigned long long *out) {
     long long c0 = clock64();
     uint64_t acc = 0;
@@ -164,6 +188,14 @@ int main() {
         cudaMemcpy(h, o, 24, cudaMemcpyDeviceToHost);
         printf("{\"globaltimer_cycles_per_read\": %.1f, \"clock64_cycles_per_read\": %.1f}\n", h[0] / 1000.0,
                h[1] / 1000.0);
+        double *io;
+        cudaMalloc(&io, 4096);
+        cudaMemset(io, 0, 4096);
+        dfma_latency<<<1, 32>>>(io, o);
+        cudaMemcpy(h, o, 24, cudaMemcpyDeviceToHost);
+        printf("{\"dfma_dep_latency_cycles\": %.1f, \"lds_chain_cycles\": %.1f, \"ffma_dep_latency_cycles\": %.1f}\n",
+               h[0] / 1000.0, h[1] / 1000.0, h[2] / 1000.0);
+        cudaFree(io);
         cudaFree(o);
     }
     for (int bg : {0, 146}) {
