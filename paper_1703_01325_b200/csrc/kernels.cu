@@ -355,8 +355,10 @@ __device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const S
 // dependencies a row has (checking each value right after its own load would
 // serialise one round trip per dependency).  Values come back untagged.
 template <int BS, int NE>
-__device__ __forceinline__ void wait_values(const double *const (&p)[NE], int64_t stride, double (&xv)[NE][BS],
+__device__ __forceinline__ void wait_values(const double *__restrict__ base, const double *__restrict__ last_base,
+                                            const int (&pos)[NE], int64_t stride, double (&xv)[NE][BS],
                                             uint32_t pend, uint32_t par, const SweepArgs &a) {
+    // entry e < NE-1 lives at base + pos[e], the last entry at last_base + pos[NE-1]
     uint64_t t0 = 0;
     uint32_t spins = 0;
 #pragma unroll
@@ -367,8 +369,9 @@ __device__ __forceinline__ void wait_values(const double *const (&p)[NE], int64_
 #pragma unroll
         for (int e = 0; e < NE; ++e)
             if (pend & (1u << e)) {
+                const double *p = (e == NE - 1 ? last_base : base) + pos[e];
 #pragma unroll
-                for (int q = 0; q < BS; ++q) xv[e][q] = ld_relaxed(p[e] + q * stride);
+                for (int q = 0; q < BS; ++q) xv[e][q] = ld_relaxed(p + q * stride);
             }
         uint32_t still = 0;
 #pragma unroll
@@ -402,7 +405,7 @@ __device__ __forceinline__ void advance_prefix(uint32_t l, const SweepArgs &a) {
 }
 
 template <int BS>
-__global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
     constexpr int R = rows_per_tile(BS);
     constexpr int BS2 = BS * BS;
     constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
@@ -499,18 +502,18 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
             for (int s0 = 0; s0 < S || (up && s0 == 0); s0 += CH) {
                 // entries 0..CH-1: dependencies of this chunk; entry CH: the
                 // row's own y_i (U' tiles, first chunk), polled in the same round
-                const double *pp[CH + 1];
+                int pp[CH + 1];
                 double xv[CH + 1][BS];
                 uint32_t pend = 0;
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
                     const int j = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
-                    pp[c] = dep + (j >= 0 ? j : 0);
+                    pp[c] = j >= 0 ? j : 0;
                     if (j >= 0) pend |= 1u << c;
                 }
-                pp[CH] = a.y_t + (up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0);
+                pp[CH] = up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0;
                 if (up && s0 == 0) pend |= 1u << CH;
-                wait_values<BS, CH + 1>(pp, npos, xv, pend, par, a);
+                wait_values<BS, CH + 1>(dep, a.y_t, pp, npos, xv, pend, par, a);
                 if (a.trace && lane == 0 && s0 == 0) {
                     tr_deps = globaltimer();
                     cyc_deps = clock64();

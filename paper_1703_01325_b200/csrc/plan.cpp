@@ -345,7 +345,7 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
         stages = 1;
         warps = int(budget / (size_t(p.stage_bytes) + 16));
     }
-    warps = std::max(1, std::min(warps, 16));
+    warps = std::max(1, std::min(warps, 8));   // <= 256 threads: the kernel keeps 255 registers
     p.sweep_stages = stages;
     p.sweep_warps = warps;
     p.sweep_ctas = num_sms;
