@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
     constexpr int R = rows_per_tile(BS);
     constexpr int BS2 = BS * BS;
     constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
+    // register-staged slots per row: ~40 doubles of matrix values (none for bs > 5)
+    constexpr bool STAGE = BS <= 5;
+    constexpr int CHR = !STAGE ? 0 : ((40 / BS2) < CH ? (40 / BS2) : CH);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int last_cta;
     __shared__ uint32_t cta_prefix;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
         // cheap wait: one lane polls ONE dependency of the previous level (one
         // 8-byte load, back-off) so that warps far ahead of the frontier do
         // not flood their SM's load pipeline with full-warp polls
-        const int probe = (a.probe == 1 || a.probe == 2) ? m.probe[a.probe - 1] : -1;
+        const int probe = a.probe == 1 ? m.probe[0] : (a.probe == 2 ? m.probe[1] : -1);
         if (lane == 0 && probe != -1) {
             const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * a.npos + probe
                                           : a.y_t + (BS - 1) * a.npos + (-probe - 2);
@@ -499,6 +502,19 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
             const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
             const double *dep = up ? a.x_t : a.y_t;
             const int64_t npos = a.npos;
+            // stage the first CHR slots' blocks (and D^-1) in registers BEFORE the
+            // poll: once the dependencies arrive only register FMAs remain
+            double vr[CHR > 0 ? CHR : 1][BS2];
+            double dr[STAGE ? BS2 : 1];
+            const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S)) + lane;
+#pragma unroll
+            for (int c = 0; c < CHR; ++c)
+#pragma unroll
+                for (int x = 0; x < BS2; ++x) vr[c][x] = c < S ? vals[(size_t(c) * BS2 + x) * R + lane] : 0.0;
+            if (STAGE && up) {
+#pragma unroll
+                for (int x = 0; x < (STAGE ? BS2 : 1); ++x) dr[x] = dv[x * R];
+            }
             for (int s0 = 0; s0 < S || (up && s0 == 0); s0 += CH) {
                 // entries 0..CH-1: dependencies of this chunk; entry CH: the
                 // row's own y_i (U' tiles, first chunk), polled in the same round
@@ -519,21 +535,43 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
                     cyc_deps = clock64();
                 }
                 if (up && s0 == 0) {
-                    const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S));
 #pragma unroll
                     for (int r = 0; r < BS; ++r) {
-                        double z = 0.0;
+                        double z = (STAGE ? dr[r % (STAGE ? BS2 : 1)] : dv[r * R]) * xv[CH][0];
 #pragma unroll
-                        for (int c = 0; c < BS; ++c) z = fma(dv[(c * BS + r) * R + lane], xv[CH][c], z);
+                        for (int c = 1; c < BS; ++c)
+                            z = fma(STAGE ? dr[(c * BS + r) % (STAGE ? BS2 : 1)] : dv[(c * BS + r) * R], xv[CH][c], z);
                         acc[r] = z;
                     }
                 }
-                // products: warp-uniform slot loop (S is per tile), padding slots hold
-                // zero blocks and zero x, so no per-lane guards; each slot is an
-                // independent short FMA chain, summed into acc in slot order
+                // products.  Padding slots hold zero blocks and zero x, so no
+                // per-lane guards.  Register-staged slots (first chunk): all
+                // CHR chains run in parallel, then a pairwise tree into acc.
+                // Remaining slots: warp-uniform loop over shared memory.
+                if (s0 == 0 && CHR > 0) {
+                    double pr[CHR > 0 ? CHR : 1][BS];
+#pragma unroll
+                    for (int c = 0; c < CHR; ++c)
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) {
+                            double p = vr[c][r] * xv[c][0];
+#pragma unroll
+                            for (int q = 1; q < BS; ++q) p = fma(vr[c][q * BS + r], xv[c][q], p);
+                            pr[c][r] = p;
+                        }
+#pragma unroll
+                    for (int w = 1; w < CHR; w <<= 1)
+#pragma unroll
+                        for (int c = 0; c + w < CHR; c += 2 * w)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r) pr[c][r] += pr[c + w][r];
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
+                }
+                const int cstart = s0 == 0 ? CHR : 0;   // first-chunk register slots are done
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
-                    if (s0 + c < S) {
+                    if (c >= cstart && s0 + c < S) {
                         const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
                         double pr[BS];
 #pragma unroll
