@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
                     for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
                 }
                 const int cstart = s0 == 0 ? CHR : 0;   // first-chunk register slots are done
+                if (s0 + cstart < S)                    // one uniform branch skips the empty tail
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
                     if (c >= cstart && s0 + c < S) {
