@@ -36,8 +36,8 @@ static DevStatus *dev_status(Plan &p) { return reinterpret_cast<DevStatus *>(p.w
 
 // the parity-tagged sweep vectors restart at parity 0 (so the next apply, parity 1, sees no stale data)
 static cudaError_t clear_tagged(Plan &p, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * plan_npos(p) * p.bs, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * plan_npos(p) * p.bs, s);
+    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * plan_npos(p) * vec_stride(p.bs), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * plan_npos(p) * vec_stride(p.bs), s);
     return e;
 }
 

@@ -45,6 +45,8 @@ BILUK_HD constexpr inline int rows_per_tile(int bs) {
     return bs <= 4 ? 32 : (bs <= 6 ? 16 : 8);
 }
 BILUK_HD constexpr inline int64_t align128(int64_t x) { return (x + 127) & ~int64_t(127); }
+// doubles per position in the sweep vectors (power of two >= bs: vector loads/stores)
+BILUK_HD constexpr inline int vec_stride(int bs) { return bs <= 1 ? 1 : (bs <= 2 ? 2 : (bs <= 4 ? 4 : 8)); }
 // header: rows int32[R] (natural block-row index, -1 = padding); U' tiles add
 // ypos int32[R] (the row's position in the L sweep, where its y lives)
 BILUK_HD constexpr inline int64_t rec_hdr_bytes(bool upper) { return upper ? 256 : 128; }
@@ -156,7 +158,8 @@ struct Op {
     bool bound = false, valued = false;
 };
 
-// component stride of the position-indexed sweep vectors y_t / x_t
+// positions of the sweep vectors y_t / x_t (each position holds one block row,
+// vec_stride(bs) contiguous doubles)
 inline int64_t plan_npos(const Plan &p) {
     const int64_t a = p.sl.ntiles * rows_per_tile(p.bs), b = p.su.ntiles * rows_per_tile(p.bs);
     return a > b ? a : b;

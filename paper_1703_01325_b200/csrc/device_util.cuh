@@ -38,6 +38,46 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// ---- vector relaxed accesses (up to 256-bit, sm_100a LDG/STG.E.256.STRONG.GPU)
+__device__ __forceinline__ void ld_relaxed_v2(const double *p, double &a, double &b) {
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0,%1}, [%2];" : "=d"(a), "=d"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v4(const double *p, double &a, double &b, double &c, double &d) {
+    asm volatile("ld.relaxed.gpu.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2(double *p, double a, double b) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v4(double *p, double a, double b, double c, double d) {
+    asm volatile("st.relaxed.gpu.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+                 : "memory");
+}
+// a block row of the sweep vectors: BS values at p (stride vec_stride(BS), aligned),
+// moved with the fewest vector instructions (4 / 2 / 1 doubles)
+template <int BS>
+__device__ __forceinline__ void ld_row(const double *p, double (&v)[BS]) {
+    constexpr int N4 = BS / 4, O2 = 4 * N4, H2 = (BS - O2) / 2, O1 = O2 + 2 * H2, H1 = BS - O1;
+#pragma unroll
+    for (int k = 0; k < N4; ++k) ld_relaxed_v4(p + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    if constexpr (H2 > 0) ld_relaxed_v2(p + O2, v[O2], v[O2 + 1]);
+    if constexpr (H1 > 0) v[O1] = ld_relaxed(p + O1);
+}
+template <int BS>
+__device__ __forceinline__ void st_row(double *p, const double (&v)[BS]) {
+    if constexpr (BS == 3) {   // pad the 4th double: one 256-bit store
+        st_relaxed_v4(p, v[0], v[1], v[2], 0.0);
+    } else {
+        constexpr int N4 = BS / 4, O2 = 4 * N4, H2 = (BS - O2) / 2, O1 = O2 + 2 * H2, H1 = BS - O1;
+#pragma unroll
+        for (int k = 0; k < N4; ++k) st_relaxed_v4(p + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        if constexpr (H2 > 0) st_relaxed_v2(p + O2, v[O2], v[O2 + 1]);
+        if constexpr (H1 > 0) st_relaxed(p + O1, v[O1]);
+    }
+}
+
 // ---- parity tags.  Every value a sweep publishes carries the apply epoch's
 // parity in its mantissa LSB (<= 1 ulp, 2^-52 relative).  A consumer polls the
 // value itself: the value is its own ready flag, so a dependency costs ONE

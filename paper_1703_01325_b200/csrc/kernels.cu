@@ -356,9 +356,10 @@ __device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const S
 // serialise one round trip per dependency).  Values come back untagged.
 template <int BS, int NE>
 __device__ __forceinline__ void wait_values(const double *__restrict__ base, const double *__restrict__ last_base,
-                                            const int (&pos)[NE], int64_t stride, double (&xv)[NE][BS],
-                                            uint32_t pend, uint32_t par, const SweepArgs &a) {
-    // entry e < NE-1 lives at base + pos[e], the last entry at last_base + pos[NE-1]
+                                            const int (&pos)[NE], double (&xv)[NE][BS], uint32_t pend, uint32_t par,
+                                            const SweepArgs &a) {
+    // entry e < NE-1 is the row at position pos[e] of base, the last entry of last_base;
+    // a row is vec_stride(BS) contiguous doubles
     uint64_t t0 = 0;
     uint32_t spins = 0;
 #pragma unroll
@@ -369,9 +370,7 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ base, con
 #pragma unroll
         for (int e = 0; e < NE; ++e)
             if (pend & (1u << e)) {
-                const double *p = (e == NE - 1 ? last_base : base) + pos[e];
-#pragma unroll
-                for (int q = 0; q < BS; ++q) xv[e][q] = ld_relaxed(p + q * stride);
+                ld_row<BS>((e == NE - 1 ? last_base : base) + int64_t(pos[e]) * vec_stride(BS), xv[e]);
             }
         uint32_t still = 0;
 #pragma unroll
@@ -484,8 +483,8 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
         // not flood their SM's load pipeline with full-warp polls
         const int probe = a.probe == 1 ? m.probe[0] : (a.probe == 2 ? m.probe[1] : -1);
         if (lane == 0 && probe != -1) {
-            const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + (BS - 1) * a.npos + probe
-                                          : a.y_t + (BS - 1) * a.npos + (-probe - 2);
+            const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + int64_t(probe) * vec_stride(BS) + (BS - 1)
+                                          : a.y_t + int64_t(-probe - 2) * vec_stride(BS) + (BS - 1);
             uint64_t t0 = 0;
             uint32_t spins = 0;
             while (tag_of(ld_relaxed(pv)) != par) {
@@ -501,7 +500,6 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
             const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
             const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
             const double *dep = up ? a.x_t : a.y_t;
-            const int64_t npos = a.npos;
             // stage the first CHR slots' blocks (and D^-1) in registers BEFORE the
             // poll: once the dependencies arrive only register FMAs remain
             double vr[CHR > 0 ? CHR : 1][BS2];
@@ -529,7 +527,7 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
                 }
                 pp[CH] = up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0;
                 if (up && s0 == 0) pend |= 1u << CH;
-                wait_values<BS, CH + 1>(dep, a.y_t, pp, npos, xv, pend, par, a);
+                wait_values<BS, CH + 1>(dep, a.y_t, pp, xv, pend, par, a);
                 if (a.trace && lane == 0 && s0 == 0) {
                     tr_deps = globaltimer();
                     cyc_deps = clock64();
@@ -586,11 +584,14 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
                     }
                 }
             }
-            if (a.trace && lane == 0) cyc_fma = clock64() + 0 * acc[0];
-            // publish at this row's own position: one coalesced store per component
-            double *dst = (up ? a.x_t : a.y_t) + (up ? t - a.nl : t) * R + lane;
+            if (a.trace && lane == 0) cyc_fma = clock64();
+            // publish the row at its own position: one (or two) vector stores,
+            // coalesced across the warp's consecutive positions
+            double *dst = (up ? a.x_t : a.y_t) + ((up ? t - a.nl : t) * R + lane) * vec_stride(BS);
+            double pub[BS];
 #pragma unroll
-            for (int r = 0; r < BS; ++r) st_relaxed(dst + r * npos, tag(acc[r], par));
+            for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
+            st_row<BS>(dst, pub);
             if (up && a.out) {
 #pragma unroll
                 for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];

@@ -373,8 +373,8 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.su_rec = take(p.su.rec_total);
     p.off.pos_l = take(4 * p.n);
     p.off.pos_u = take(4 * p.n);
-    p.off.y_t = take(8 * plan_npos(p) * p.bs);   // component-major at L positions
-    p.off.x_t = take(8 * plan_npos(p) * p.bs);   // component-major at U' positions
+    p.off.y_t = take(8 * plan_npos(p) * vec_stride(p.bs));   // rows at L positions
+    p.off.x_t = take(8 * plan_npos(p) * vec_stride(p.bs));   // rows at U' positions
     p.off.lvl_tiles = take(4 * p.lvl_tiles.size());
     p.off.lvl_cnt = take(4 * p.lvl_tiles.size());
     p.off.status = take(sizeof(DevStatus));
