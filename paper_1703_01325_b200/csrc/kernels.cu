@@ -403,14 +403,111 @@ __device__ __forceinline__ void advance_prefix(uint32_t l, const SweepArgs &a) {
     }
 }
 
+// One lane's block row of a tile: poll its dependencies (CH per round) and
+// accumulate  acc -= sum_s B_s x_s  (U' rows first set acc = D^-1 y_i).
+// The first CHR slots' blocks and D^-1 are staged in registers BEFORE the
+// poll, so once the dependencies arrive only register FMAs remain; padding
+// slots hold zero blocks and zero x, so no per-lane guards are needed.
+template <int BS, int CH, int CHR>
+__device__ __forceinline__ void row_solve(const SweepArgs &a, const unsigned char *rec, int S, bool up, int lane,
+                                          uint32_t par, double (&acc)[BS], uint64_t &tr_deps, long long &cyc_deps) {
+    constexpr int R = rows_per_tile(BS);
+    constexpr int BS2 = BS * BS;
+    constexpr bool STAGE = BS <= 4;
+    const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
+    const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
+    const double *dep = up ? a.x_t : a.y_t;
+    double vr[CHR > 0 ? CHR : 1][BS2];
+    double dr[STAGE ? BS2 : 1];
+    const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S)) + lane;
+#pragma unroll
+    for (int c = 0; c < CHR; ++c)
+#pragma unroll
+        for (int x = 0; x < BS2; ++x) vr[c][x] = c < S ? vals[(size_t(c) * BS2 + x) * R + lane] : 0.0;
+    if (STAGE && up) {
+#pragma unroll
+        for (int x = 0; x < (STAGE ? BS2 : 1); ++x) dr[x] = dv[x * R];
+    }
+    for (int s0 = 0; s0 < S || (up && s0 == 0); s0 += CH) {
+        // entries 0..CH-1: dependencies of this chunk; entry CH: the row's own
+        // y_i (U' tiles, first chunk), polled in the same round
+        int pp[CH + 1];
+        double xv[CH + 1][BS];
+        uint32_t pend = 0;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int j = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
+            pp[c] = j >= 0 ? j : 0;
+            if (j >= 0) pend |= 1u << c;
+        }
+        pp[CH] = up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0;
+        if (up && s0 == 0) pend |= 1u << CH;
+        wait_values<BS, CH + 1>(dep, a.y_t, pp, xv, pend, par, a);
+        if (a.trace && lane == 0 && s0 == 0) {
+            tr_deps = globaltimer();
+            cyc_deps = clock64();
+        }
+        if (up && s0 == 0) {
+#pragma unroll
+            for (int r = 0; r < BS; ++r) {
+                double z = (STAGE ? dr[r % (STAGE ? BS2 : 1)] : dv[r * R]) * xv[CH][0];
+#pragma unroll
+                for (int c = 1; c < BS; ++c)
+                    z = fma(STAGE ? dr[(c * BS + r) % (STAGE ? BS2 : 1)] : dv[(c * BS + r) * R], xv[CH][c], z);
+                acc[r] = z;
+            }
+        }
+        // register-staged slots (first chunk): all chains in parallel, then a
+        // pairwise tree into acc; remaining slots: warp-uniform shared-memory loop
+        if (s0 == 0 && CHR > 0) {
+            double pr[CHR > 0 ? CHR : 1][BS];
+#pragma unroll
+            for (int c = 0; c < CHR; ++c)
+#pragma unroll
+                for (int r = 0; r < BS; ++r) {
+                    double p = vr[c][r] * xv[c][0];
+#pragma unroll
+                    for (int q = 1; q < BS; ++q) p = fma(vr[c][q * BS + r], xv[c][q], p);
+                    pr[c][r] = p;
+                }
+#pragma unroll
+            for (int w = 1; w < CHR; w <<= 1)
+#pragma unroll
+                for (int c = 0; c + w < CHR; c += 2 * w)
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) pr[c][r] += pr[c + w][r];
+#pragma unroll
+            for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
+        }
+        const int cstart = s0 == 0 ? CHR : 0;
+        if (s0 + cstart < S)
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                if (c >= cstart && s0 + c < S) {
+                    const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
+                    double pr[BS];
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) pr[r] = v[r * R] * xv[c][0];
+#pragma unroll
+                    for (int q = 1; q < BS; ++q)
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) pr[r] = fma(v[(q * BS + r) * R], xv[c][q], pr[r]);
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] -= pr[r];
+                }
+            }
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
     constexpr int R = rows_per_tile(BS);
     constexpr int BS2 = BS * BS;
     constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
     // register-staged slots per row: ~40 doubles of matrix values (none for bs > 5)
-    constexpr bool STAGE = BS <= 5;
-    constexpr int CHR = !STAGE ? 0 : ((40 / BS2) < CH ? (40 / BS2) : CH);
+    constexpr int CHR = BS > 4 ? 0 : (BS == 4 ? 1 : ((40 / BS2) < CH ? (40 / BS2) : CH));
+    constexpr int CHS = BS <= 3 ? 4 : (BS <= 4 ? 2 : 1);   // narrow-tile poll width
+    constexpr int CHS_R = CHR < CHS ? CHR : CHS;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int last_cta;
     __shared__ uint32_t cta_prefix;
@@ -497,93 +594,12 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
         long long cyc_deps = 0, cyc_fma = 0, cyc_st = 0;
         if (a.trace && lane == 0) tr1 = globaltimer();
         if (row >= 0) {
-            const int *cols = reinterpret_cast<const int *>(rec + rec_hdr_bytes(up));
-            const double *vals = reinterpret_cast<const double *>(rec + rec_vals_off(BS, S, up));
-            const double *dep = up ? a.x_t : a.y_t;
-            // stage the first CHR slots' blocks (and D^-1) in registers BEFORE the
-            // poll: once the dependencies arrive only register FMAs remain
-            double vr[CHR > 0 ? CHR : 1][BS2];
-            double dr[STAGE ? BS2 : 1];
-            const double *dv = reinterpret_cast<const double *>(rec + rec_dinv_off(BS, S)) + lane;
-#pragma unroll
-            for (int c = 0; c < CHR; ++c)
-#pragma unroll
-                for (int x = 0; x < BS2; ++x) vr[c][x] = c < S ? vals[(size_t(c) * BS2 + x) * R + lane] : 0.0;
-            if (STAGE && up) {
-#pragma unroll
-                for (int x = 0; x < (STAGE ? BS2 : 1); ++x) dr[x] = dv[x * R];
-            }
-            for (int s0 = 0; s0 < S || (up && s0 == 0); s0 += CH) {
-                // entries 0..CH-1: dependencies of this chunk; entry CH: the
-                // row's own y_i (U' tiles, first chunk), polled in the same round
-                int pp[CH + 1];
-                double xv[CH + 1][BS];
-                uint32_t pend = 0;
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const int j = (s0 + c < S) ? cols[(s0 + c) * R + lane] : -1;
-                    pp[c] = j >= 0 ? j : 0;
-                    if (j >= 0) pend |= 1u << c;
-                }
-                pp[CH] = up ? reinterpret_cast<const int *>(rec + 128)[lane] : 0;
-                if (up && s0 == 0) pend |= 1u << CH;
-                wait_values<BS, CH + 1>(dep, a.y_t, pp, xv, pend, par, a);
-                if (a.trace && lane == 0 && s0 == 0) {
-                    tr_deps = globaltimer();
-                    cyc_deps = clock64();
-                }
-                if (up && s0 == 0) {
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) {
-                        double z = (STAGE ? dr[r % (STAGE ? BS2 : 1)] : dv[r * R]) * xv[CH][0];
-#pragma unroll
-                        for (int c = 1; c < BS; ++c)
-                            z = fma(STAGE ? dr[(c * BS + r) % (STAGE ? BS2 : 1)] : dv[(c * BS + r) * R], xv[CH][c], z);
-                        acc[r] = z;
-                    }
-                }
-                // products.  Padding slots hold zero blocks and zero x, so no
-                // per-lane guards.  Register-staged slots (first chunk): all
-                // CHR chains run in parallel, then a pairwise tree into acc.
-                // Remaining slots: warp-uniform loop over shared memory.
-                if (s0 == 0 && CHR > 0) {
-                    double pr[CHR > 0 ? CHR : 1][BS];
-#pragma unroll
-                    for (int c = 0; c < CHR; ++c)
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) {
-                            double p = vr[c][r] * xv[c][0];
-#pragma unroll
-                            for (int q = 1; q < BS; ++q) p = fma(vr[c][q * BS + r], xv[c][q], p);
-                            pr[c][r] = p;
-                        }
-#pragma unroll
-                    for (int w = 1; w < CHR; w <<= 1)
-#pragma unroll
-                        for (int c = 0; c + w < CHR; c += 2 * w)
-#pragma unroll
-                            for (int r = 0; r < BS; ++r) pr[c][r] += pr[c + w][r];
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
-                }
-                const int cstart = s0 == 0 ? CHR : 0;   // first-chunk register slots are done
-                if (s0 + cstart < S)                    // one uniform branch skips the empty tail
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    if (c >= cstart && s0 + c < S) {
-                        const double *v = vals + size_t(s0 + c) * BS2 * R + lane;
-                        double pr[BS];
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) pr[r] = v[r * R] * xv[c][0];
-#pragma unroll
-                        for (int q = 1; q < BS; ++q)
-#pragma unroll
-                            for (int r = 0; r < BS; ++r) pr[r] = fma(v[(q * BS + r) * R], xv[c][q], pr[r]);
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) acc[r] -= pr[r];
-                    }
-                }
-            }
+            // narrow tiles (<= CHS dependency slots, e.g. every ILU(0) row) use a
+            // poll of CHS entries; wider ones the general CH-wide chunked poll
+            if (S <= CHS)
+                row_solve<BS, CHS, CHS_R>(a, rec, S, up, lane, par, acc, tr_deps, cyc_deps);
+            else
+                row_solve<BS, CH, CHR>(a, rec, S, up, lane, par, acc, tr_deps, cyc_deps);
             if (a.trace && lane == 0) cyc_fma = clock64();
             // publish the row at its own position: one (or two) vector stores,
             // coalesced across the warp's consecutive positions
