@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -36,8 +37,8 @@ static DevStatus *dev_status(Plan &p) { return reinterpret_cast<DevStatus *>(p.w
 
 // the parity-tagged sweep vectors restart at parity 0 (so the next apply, parity 1, sees no stale data)
 static cudaError_t clear_tagged(Plan &p, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * plan_npos(p) * vec_stride(p.bs), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * plan_npos(p) * vec_stride(p.bs), s);
+    cudaError_t e = cudaMemsetAsync(p.ws + p.off.y_t, 0, 8 * plan_npos(p) * plan_vs(p), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.ws + p.off.x_t, 0, 8 * plan_npos(p) * plan_vs(p), s);
     return e;
 }
 
@@ -130,7 +131,29 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     } else {
         cudaGetLastError();   // no device here: plan for a B200
     }
-    plan_layout(h->p, sms, size_t(smem));
+    // apply engine: the partitioned sweep; the tiled level-order sweep only
+    // for patterns the partitioned one cannot stage (very long block rows)
+    Plan &P = h->p;
+    P.engine = 1;
+    if (const char *env = std::getenv("BILUK_ENGINE")) P.engine = std::atoi(env) == 0 ? 0 : 1;
+    if (P.engine == 1) {
+        rc = plan_psweep(P, sms, size_t(smem), 0);
+        if (rc == BILUK_EUNSUPPORTED) {
+            P.engine = 0;
+            P.ps = PSweep{};
+        } else if (rc != BILUK_OK) {
+            delete h;
+            return rc;
+        }
+    }
+    if (P.engine == 0) {
+        rc = plan_tiles(P);
+        if (rc != BILUK_OK) {
+            delete h;
+            return rc;
+        }
+    }
+    plan_layout(P, sms, size_t(smem));
     *out = h;
     return BILUK_OK;
 }
@@ -148,7 +171,11 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     p.ws = static_cast<unsigned char *>(dev_workspace);
     // launch configuration check: the persistent sweep needs every CTA resident
     int per_sm = 0;
-    CUDA_TRY(sweep_occupancy(p, &per_sm), "sweep occupancy");
+    if (p.engine == 1) {
+        CUDA_TRY(psweep_occupancy(p, &per_sm), "sweep occupancy");
+    } else {
+        CUDA_TRY(sweep_occupancy(p, &per_sm), "sweep occupancy");
+    }
     if (per_sm < 1) return fail(BILUK_EUNSUPPORTED, "sweep kernel does not fit on an SM");
     auto up = [&](uint64_t off, const void *src, size_t n) -> cudaError_t {
         if (n == 0) return cudaSuccess;
@@ -165,6 +192,11 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     CUDA_TRY(up(p.off.su_meta, p.su.meta.data(), sizeof(TileMeta) * p.su.meta.size()), "upload");
     CUDA_TRY(up(p.off.lvl_tiles, p.lvl_tiles.data(), 4 * p.lvl_tiles.size()), "upload");
     CUDA_TRY(cudaMemsetAsync(p.ws + p.off.lvl_cnt, 0, 4 * p.lvl_tiles.size(), s), "memset");
+    CUDA_TRY(up(p.off.ps_info, p.ps.rec.data(), sizeof(PRecInfo) * p.ps.rec.size()), "upload");
+    CUDA_TRY(up(p.off.ps_part, p.ps.part_rec.data(), 4 * p.ps.part_rec.size()), "upload");
+    CUDA_TRY(up(p.off.ps_idx, p.ps.idx.data(), 4 * p.ps.idx.size()), "upload");
+    CUDA_TRY(up(p.off.ps_vmap, p.ps.vmap.data(), 4 * p.ps.vmap.size()), "upload");
+    if (p.engine == 1) CUDA_TRY(up(p.off.ps_posl, p.ps.posL.data(), 4 * p.ps.posL.size()), "upload");
     CUDA_TRY(up(p.off.pos_l, p.sl.pos.data(), 4 * p.sl.pos.size()), "upload");
     CUDA_TRY(up(p.off.pos_u, p.su.pos.data(), 4 * p.su.pos.size()), "upload");
     // parity-tagged vectors start at parity 0 everywhere; the first apply uses parity 1
@@ -203,7 +235,11 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
         return fail(BILUK_ESINGULAR, "singular diagonal block at row " + std::to_string(h.ferr_row));
     }
     CUDA_TRY(launch_split(p, s), "split");
-    CUDA_TRY(launch_pack(p, s), "pack");
+    if (p.engine == 1) {
+        CUDA_TRY(launch_ppack(p, s), "pack");
+    } else {
+        CUDA_TRY(launch_pack(p, s), "pack");
+    }
     CUDA_TRY(cudaStreamSynchronize(s), "pack sync");
     p.factored = true;
     return BILUK_OK;
@@ -214,6 +250,28 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     Plan &p = plan->p;
     if (p.n == 0) return BILUK_OK;
     if (dev_b == dev_x) return fail(BILUK_EARG, "output may not alias the right-hand side");
+    if (p.engine == 1) {
+        PSweepArgs a{};
+        a.rec = reinterpret_cast<const PRecInfo *>(p.ws + p.off.ps_info);
+        a.recs = p.ws + p.off.ps_rec;
+        a.part_rec = reinterpret_cast<const int32_t *>(p.ws + p.off.ps_part);
+        a.b = dev_b;
+        a.y_t = reinterpret_cast<double *>(p.ws + p.off.y_t);
+        a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
+        a.out = dev_x;
+        a.st = dev_status(p);
+        a.skip_flag = nullptr;
+        a.timeout_ns = 2000000000ull;
+        a.ring_mask = p.ps.ring - 1;
+        a.data_bytes = uint32_t(p.ps.data_ring);
+        a.trace = p.trace;
+        a.nrec_total = int64_t(p.ps.rec.size());
+        a.b_perm = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
+        a.y_u = reinterpret_cast<double *>(p.ws + p.off.ps_yu);
+        CUDA_TRY(launch_permute_b(p, dev_b, static_cast<cudaStream_t>(stream)), "apply");
+        CUDA_TRY(launch_psweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+        return BILUK_OK;
+    }
     SweepArgs a{};
     a.meta_l = reinterpret_cast<const TileMeta *>(p.ws + p.off.sl_meta);
     a.meta_u = reinterpret_cast<const TileMeta *>(p.ws + p.off.su_meta);
@@ -308,7 +366,9 @@ int biluk_plan_info(const biluk_plan_t *plan, int64_t *info, int32_t ninfo) {
                          p.nL,         p.nU,         p.nlev_L,      p.nlev_U,        p.sl.ntiles,
                          p.su.ntiles,  rows_per_tile(p.bs), int64_t(p.off.total), apply_bytes(p), spmv_bytes(p),
                          p.sweep_ctas, p.sweep_warps, p.sweep_stages, p.stage_bytes,
-                         std::max(p.sl.max_slots, p.su.max_slots)};
+                         std::max(p.sl.max_slots, p.su.max_slots), p.engine, p.ps.P,
+                         int64_t(p.ps.rec.size()), int64_t(p.ps.est_us * 1000.0), p.ps.rec_total,
+                         p.ps.nglob_total, p.ps.partition, p.ps.split[0], p.ps.split[1]};
     const int nv = int(sizeof(v) / sizeof(v[0]));
     for (int i = 0; i < ninfo; ++i) info[i] = i < nv ? v[i] : 0;
     return BILUK_OK;

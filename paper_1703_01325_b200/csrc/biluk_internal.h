@@ -109,6 +109,92 @@ struct Sweep {                       // host copy of one sweep's tile layout
     int64_t max_rec = 0;
 };
 
+// ---------------------------------------------------------------------------
+// Partitioned sweep (the apply engine).
+//
+// The block rows are cut into P contiguous ranges ("parts"), one CTA each.
+// Every L dependency of a row lies in its own part or an EARLIER part, every
+// U' dependency in its own part or a LATER one, so the parts form a chain and
+// the level chain mostly stays inside one SM: a dependency on the same part
+// is read from a shared-memory ring of recent results, one on another part is
+// fetched (parity-tag polled) from L2 by a prefetch warp ahead of use.
+// A part's rows are processed in (global level, row) order, one thread per
+// row, in RECORDS of <= nthreads rows of one level; a record is one
+// contiguous byte range moved by one cp.async.bulk:
+//   hdr   PRecHdr (32 B)
+//   iarr  int32[nrows]          L: the row's U' position (where it stores y for
+//                               the U' sweep); U': natural block row (x scatter)
+//   desc  int32[S][nrows]       >= 0: vector-ring slot (slot `ring` is zero);
+//                               < 0: fetched dependency -(d+1)
+//   gpos  int32[nglob]          deduplicated dependency positions in the
+//                               sweep's own vector (parity-tag polled)
+//   (align 16)
+//   dinv  f64[bs*bs][nrows]     U' only
+//   vals  f64[S][bs*bs][nrows]  element e = c*bs + r (column-major blocks)
+//   (align 16)                  = `bytes`, streamed by one bulk copy
+// and, in shared memory only, behind it:
+//   input f64[nrows][pvs]       the rows' own inputs, a second bulk copy of
+//                               the position-ordered b (L) or y (U') vector
+//   deps  f64[bs][nglob]        fetched dependencies, component-major
+// ---------------------------------------------------------------------------
+struct PRecHdr {        // 32 bytes
+    int32_t nrows, S, nglob;
+    int32_t flags;      // bit 0: U' record; bits 1..: dependency level (diagnostics)
+    int32_t seq0;       // ring sequence number of the first row
+    int32_t pos0;       // vector position of the first row (y_t for L, x_t for U')
+    int32_t vals_off;   // byte offset of dinv (U') / vals inside the record
+    int32_t in_off;     // byte offset of the input area (= record bytes); deps follow the inputs
+};
+struct PRecInfo {       // 64 bytes: one per record, read by the producer, the gather warp and the pack kernel
+    uint64_t off;       // byte offset of the record (16-aligned)
+    uint64_t idx_off;   // int32 offset of its index section in the compact index image (16-aligned)
+    int64_t vmap_off;   // first entry of its value map (S * nrows P' slots, -1 = padding)
+    uint32_t bytes;     // streamed record bytes (multiple of 16) = offset of the value area
+    uint32_t idx_words; // int32 words of the index section (header .. gpos)
+    int32_t nrows, S;
+    uint32_t foot;      // shared-memory footprint: bytes + value area
+    int32_t level;      // dependency level of its rows * 2 + upper (= PRecHdr::flags)
+    int32_t nglob;      // fetched dependencies
+    int32_t pos0;       // vector position of its first row (inputs: pos0 .. pos0 + nrows)
+    int32_t pad[2];
+};
+// doubles per position of the partitioned sweep's vectors (>= 2: 16-byte rows)
+BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
+constexpr int PS_GLOB_CAP = 128;   // fetched dependencies per record (one per prefetch thread)
+constexpr int PS_KSLOTS = 16;      // records in flight per CTA (mbarrier sets)
+
+// an assignment of block rows to parts (any assignment is deadlock-free:
+// every CTA walks its rows in global level order)
+struct Partition {
+    int P = 0;
+    int kind = 0;                    // 0: contiguous row ranges, 1: structured-grid (y, z) columns
+    int64_t grid[3] = {0, 0, 0};     // nx, ny, nz (kind 1)
+    int split[2] = {0, 0};           // parts along y, z (kind 1)
+    std::vector<int32_t> part_of;    // n
+    std::vector<std::vector<int32_t>> rows;   // rows of each part, ascending
+    std::vector<int32_t> base;       // P+1 first vector position of each part
+};
+
+struct PSweep {
+    int32_t P = 0;                   // parts = CTAs
+    int32_t partition = 0;           // Partition::kind
+    int64_t grid[3] = {0, 0, 0};
+    int32_t split[2] = {0, 0};
+    int32_t nthreads = 128;          // compute threads per CTA (+ one prefetch warp)
+    int32_t ring = 1024;             // vector ring rows (power of two; slot `ring` is all zeros)
+    int64_t data_ring = 0;           // shared-memory bytes of the record ring
+    int64_t xval_ring = 0;           // shared-memory bytes of the fetched-value ring
+    int64_t rec_cap = 0, glob_cap = 0;
+    int32_t nlrec_max = 0;           // most L records of one part
+    std::vector<int32_t> part_rec;   // P+1 record ranges (a part's L records, then its U' records)
+    std::vector<PRecInfo> rec;
+    std::vector<int32_t> idx;        // compact index sections
+    std::vector<int32_t> vmap;       // value maps
+    std::vector<int32_t> posL, posU; // vector position of every block row in each sweep
+    int64_t rec_total = 0, max_rec = 0, max_glob = 0, nglob_total = 0;
+    double est_us = 0;               // planner's time estimate for the chosen P
+};
+
 struct Plan {
     int32_t bs = 0, k = 0;
     int64_t n = 0;
@@ -124,6 +210,8 @@ struct Plan {
     std::vector<int64_t> fptr;       // level pointers into forder (nlev_L + 1)
     int32_t max_row_len = 0;         // longest P' row (factor shared memory)
     Sweep sl, su;                    // L sweep, U' sweep
+    PSweep ps;                       // partitioned sweep layout
+    int32_t engine = 1;              // 1: partitioned sweep, 0: tiled level-order sweep
     std::vector<uint32_t> lvl_tiles; // tiles per combined level (L levels, then U' levels), 1-based
     SweepTune tune;
     unsigned long long *trace = nullptr;   // optional per-tile timing records (diagnostics)
@@ -134,7 +222,8 @@ struct Plan {
     // workspace layout (byte offsets)
     struct {
         uint64_t p_rp, p_ci, p_diag, a2p, forder, pvals, dinv, sl_rows, sl_meta, sl_rec, su_rows, su_meta,
-            su_rec, pos_l, pos_u, y_t, x_t, lvl_tiles, lvl_cnt, status, total;
+            su_rec, pos_l, pos_u, y_t, x_t, lvl_tiles, lvl_cnt, status, ps_rec, ps_info, ps_part, ps_idx,
+            ps_vmap, ps_posl, ps_bperm, ps_yu, total;
     } off{};
     // bound device pointers
     unsigned char *ws = nullptr;
@@ -162,7 +251,12 @@ struct Op {
 // vec_stride(bs) contiguous doubles)
 inline int64_t plan_npos(const Plan &p) {
     const int64_t a = p.sl.ntiles * rows_per_tile(p.bs), b = p.su.ntiles * rows_per_tile(p.bs);
-    return a > b ? a : b;
+    const int64_t m = a > b ? a : b;
+    return m > p.n ? m : p.n;
+}
+// doubles per position of the sweep vectors y_t / x_t (either engine)
+inline int plan_vs(const Plan &p) {
+    return p.engine == 1 ? ps_vec_stride(p.bs) : vec_stride(p.bs);
 }
 
 // host planner (plan.cpp)
@@ -171,7 +265,12 @@ int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::
 void level_schedule(int64_t m, const int64_t *rp, const int64_t *ci, bool upper, int64_t *lev, int64_t *nlev);
 int validate_bsr(int64_t n, int64_t ncols, const int64_t *rp, const int64_t *ci);
 int plan_analyse(Plan &p, int32_t bs, int64_t n, const int64_t *rp, const int64_t *ci, int32_t k, int64_t *err_row);
+int plan_tiles(Plan &p);
 void plan_layout(Plan &p, int num_sms, size_t smem_per_sm);
+// partitioned sweep planner (psweep_plan.cpp): parts = 0 chooses P by the cost model
+int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts);
+double psweep_estimate_us(const Plan &p, const Partition &pt);
+bool detect_grid(const Plan &p, int64_t g[3]);
 int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, const int64_t *ci);
 
 }  // namespace biluk

@@ -37,6 +37,31 @@ struct SweepArgs {
     int trace_mode;              // 1: t_deps in the 4th word; 2: packed cycle splits after the poll
 };
 
+// partitioned sweep (psweep.cu)
+struct PSweepArgs {
+    const PRecInfo *rec;         // all records (a CTA's range: part_rec[c] .. part_rec[c+1])
+    const unsigned char *recs;   // record bytes
+    const int32_t *part_rec;     // P+1
+    const double *b;             // right-hand side (n*bs, natural order)
+    double *y_t;                 // parity-tagged y at L positions (vec_stride(bs) doubles each)
+    double *x_t;                 // parity-tagged x at U' positions
+    double *out;                 // untagged x (natural order; may be null)
+    DevStatus *st;
+    const int *skip_flag;        // when non-null and *skip_flag != 0 the launch is a no-op
+    uint64_t timeout_ns;
+    int ring_mask;               // vector ring rows - 1 (slot ring_mask+1 holds zeros)
+    uint32_t data_bytes;         // record ring bytes
+    unsigned long long *trace;   // optional: 8 x u64 per record (globaltimer stamps), then diagnostics
+    int64_t nrec_total;
+    const double *b_perm;        // b in L-position order (pvs doubles per position; launch_permute_b)
+    double *y_u;                 // y in U'-position order (written by the L sweep, read by U' records)
+};
+cudaError_t launch_ppack(const Plan &p, cudaStream_t s);
+cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s);
+cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s);
+cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm);
+size_t psweep_smem_bytes(const Plan &p);
+
 cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);
 cudaError_t launch_factor(const Plan &p, cudaStream_t s);
 cudaError_t launch_split(const Plan &p, cudaStream_t s);

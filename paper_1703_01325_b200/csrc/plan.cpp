@@ -264,6 +264,11 @@ int plan_analyse(Plan &p, int32_t bs, int64_t n, const int64_t *rp, const int64_
         for (int l = 1; l <= p.nlev_L; ++l) cur[l] = p.fptr[l - 1];
         for (int64_t i = 0; i < n; ++i) p.forder[cur[p.lev_L[i]]++] = int32_t(i);
     }
+    return BILUK_OK;
+}
+
+// tile layout of the level-order engine (engine 0)
+int plan_tiles(Plan &p) {
     build_sweep(p, false, p.lev_L, p.nlev_L, p.sl, nullptr);
     build_sweep(p, true, p.lev_U, p.nlev_U, p.su, &p.sl);
     // tiles per combined level: L levels 1..nlev_L, then U' levels nlev_L+1..
@@ -337,6 +342,12 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     // sweep launch: one CTA per SM holding as many warps as the double-buffered
     // tile ring allows (each warp owns `stages` stage buffers of the largest record)
     p.num_sms = num_sms;
+    if (p.engine == 1) {
+        p.sweep_ctas = p.ps.P;
+        p.sweep_warps = 2 * p.ps.nthreads / 32 + 4;   // two compute groups + producer, gather, 2 poll
+        p.sweep_stages = PS_KSLOTS;
+        p.stage_bytes = p.ps.max_rec;
+    } else {
     p.stage_bytes = std::max<int64_t>(128, std::max(p.sl.max_rec, p.su.max_rec));
     const size_t budget = smem_per_sm > 8192 ? smem_per_sm - 4096 : smem_per_sm;
     int stages = 2;
@@ -349,6 +360,7 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.sweep_stages = stages;
     p.sweep_warps = warps;
     p.sweep_ctas = num_sms;
+    }
 
     const int64_t bs2 = int64_t(p.bs) * p.bs;
     uint64_t o = 0;
@@ -373,11 +385,20 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.su_rec = take(p.su.rec_total);
     p.off.pos_l = take(4 * p.n);
     p.off.pos_u = take(4 * p.n);
-    p.off.y_t = take(8 * plan_npos(p) * vec_stride(p.bs));   // rows at L positions
-    p.off.x_t = take(8 * plan_npos(p) * vec_stride(p.bs));   // rows at U' positions
+    p.off.y_t = take(8 * plan_npos(p) * plan_vs(p));   // rows at L positions
+    p.off.x_t = take(8 * plan_npos(p) * plan_vs(p));   // rows at U' positions
     p.off.lvl_tiles = take(4 * p.lvl_tiles.size());
     p.off.lvl_cnt = take(4 * p.lvl_tiles.size());
     p.off.status = take(sizeof(DevStatus));
+    p.off.ps_rec = take(p.ps.rec_total);
+    p.off.ps_info = take(sizeof(PRecInfo) * p.ps.rec.size());
+    p.off.ps_part = take(4 * p.ps.part_rec.size());
+    p.off.ps_idx = take(4 * p.ps.idx.size());
+    p.off.ps_vmap = take(4 * p.ps.vmap.size());
+    const bool ps_on = p.engine == 1;
+    p.off.ps_posl = take(ps_on ? 4 * p.n : 0);                               // row -> L position
+    p.off.ps_bperm = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);        // b in L-position order
+    p.off.ps_yu = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);           // y in U'-position order
     p.off.total = o;
 }
 

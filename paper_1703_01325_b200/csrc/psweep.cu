@@ -1,0 +1,620 @@
+// The apply engine: a persistent, partitioned, sync-free sweep for
+//   L y = b,  z = D^-1 y,  U' x = z      (apply_preconditioner, trisolve.py:121-182)
+// and the device pack of its records from the factors.
+//
+// One CTA per part (a contiguous block-row range, psweep_plan.cpp), all CTAs
+// co-resident (cooperative launch).  Inside a CTA:
+//   * warp NW (the last one) is the PRODUCER + PREFETCHER: lane 0 streams the
+//     part's records into a shared-memory ring with cp.async.bulk (1-D TMA,
+//     evict-first), and the warp fetches every value a record needs from
+//     global memory -- the rows' own inputs (b for L, y for U') and every
+//     dependency that is not in the on-chip ring (other parts, or rows of this
+//     part that left the ring) -- polling the parity tags, into a second ring;
+//   * warps 0..NW-1 COMPUTE, one thread per block row of the record:
+//       L :  y_i = b_i - sum_j L_ij y_j
+//       U':  x_i = D_i^-1 y_i - sum_j U'_ij x_j
+//     reading dependencies from shared memory only (the vector ring of this
+//     part's recent results, or the fetched values), then publish the row to
+//     the ring, to the parity-tagged global vector (other parts poll it) and,
+//     for U', to the caller's x.  A named barrier ends every record.
+// L dependencies live in this or EARLIER parts, U' dependencies in this or
+// LATER parts (and y_i in this part): part 0's L and part P-1's U' never wait
+// on another part, so by induction every CTA finishes (no deadlock).
+#include <cstdint>
+
+#include "biluk_internal.h"
+#include "device_util.cuh"
+#include "kernels.cuh"
+
+namespace biluk {
+
+using namespace dev;
+
+namespace {
+
+constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
+constexpr int PS_NT = 2 * PS_NG;      // compute threads: two ping-pong groups
+constexpr int PS_NW = PS_NT / 32;     // compute warps; then producer, gather, poll warps
+constexpr int PS_NPOLL = 2;           // poll warps (alternate records)
+constexpr int PS_NAUX = 1 + PS_NPOLL; // producer + poll warps
+constexpr int PS_PF = 16;             // records prefetched into L2 ahead of their bulk copy
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// circular allocation of `sz` bytes in a ring of `cap` bytes whose oldest
+// live allocation starts at `tail` (`live` allocations outstanding, the next
+// free byte is `head`); returns the offset or -1
+__device__ __forceinline__ int64_t ring_alloc(uint32_t &head, uint32_t tail, int live, uint32_t sz, uint32_t cap) {
+    if (live == 0) {
+        head = sz;
+        return 0;
+    }
+    if (head > tail) {
+        if (head + sz <= cap) {
+            const uint32_t at = head;
+            head += sz;
+            return at;
+        }
+        if (sz <= tail) {
+            head = sz;
+            return 0;
+        }
+        return -1;
+    }
+    if (head < tail && head + sz <= tail) {
+        const uint32_t at = head;
+        head += sz;
+        return at;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ bool ps_timed_out(uint64_t &t0, uint32_t &spins, const PSweepArgs &a) {
+    ++spins;
+    if (spins == 1) {
+        t0 = uint64_t(clock64());
+    } else if ((spins & 255u) == 0) {
+        if (uint64_t(clock64()) - t0 > 2 * a.timeout_ns || ld_relaxed_s32(&a.st->status) != 0) {
+            atomicCAS(&a.st->status, 0, int(BILUK_ETIMEOUT));
+            return true;
+        }
+    }
+    return false;
+}
+
+}  // namespace
+
+__device__ __forceinline__ void cp_async_8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// non-blocking probe of an mbarrier phase (try_wait may suspend the thread)
+__device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// wait for an mbarrier phase; false if the sweep was aborted meanwhile or the
+// wait exceeded the timeout (which then aborts the sweep: sticky status)
+__device__ __forceinline__ bool mbar_wait_or_abort(uint64_t *bar, uint32_t phase, int *abort_flag, const PSweepArgs &a) {
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, phase)) {
+        if (*reinterpret_cast<volatile int *>(abort_flag)) return false;
+        if (ps_timed_out(t0, spins, a)) {
+            *reinterpret_cast<volatile int *>(abort_flag) = 1;
+            return false;
+        }
+    }
+    return true;
+}
+
+template <int BS>
+__global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const PSweepArgs a) {
+    constexpr int BS2 = BS * BS;
+    constexpr int VS = ps_vec_stride(BS);
+    constexpr int K = PS_KSLOTS;
+    constexpr int EPL = PS_GLOB_CAP / 32;   // dependency entries per poll lane
+    static_assert(K % PS_NPOLL == 0, "poll warps must own whole ring slots");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full_bar[K];    // record bytes + inputs landed (two bulk copies)
+    __shared__ __align__(8) uint64_t dep_bar[K];     // dependencies fetched (poll warp)
+    __shared__ __align__(8) uint64_t empty_bar[K];   // record consumed (every thread of a compute group)
+    __shared__ uint32_t slot_off[K];
+    __shared__ int abort_flag;   // a wait timed out somewhere (the device status is sticky)
+    __shared__ int last_cta;
+    if (a.skip_flag && ld_relaxed_s32(a.skip_flag) != 0) return;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double *vring = reinterpret_cast<double *>(smem);
+    unsigned char *dring = smem + size_t(a.ring_mask + 2) * VS * 8;
+    const int r0 = a.part_rec[blockIdx.x], nrec = a.part_rec[blockIdx.x + 1] - r0;
+    const uint32_t par = ld_relaxed_u32(&a.st->epoch) & 1u;
+
+    if (tid == 0) {
+        for (int s = 0; s < K; ++s) {
+            mbar_init(full_bar + s, 1);
+            mbar_init(dep_bar + s, 1);
+            mbar_init(empty_bar + s, PS_NG);
+        }
+        abort_flag = 0;
+        fence_mbar_init();
+    }
+    // vector ring, component-major: component c of slot k at vring[c * RS + k]; slot ring_mask+1 is zero
+    const int RS = a.ring_mask + 2;
+    for (int x = tid; x < VS; x += blockDim.x) vring[size_t(x) * RS + a.ring_mask + 1] = 0.0;
+    __syncthreads();
+
+    if (warp == PS_NW) {
+        // ============ producer: bulk copies into the record ring ===============
+        // per record two bulk copies on one mbarrier: the record's bytes and
+        // its rows' inputs (positions pos0 .. pos0+nr of b_perm for L, of y_u
+        // for U' -- the latter only once this part's L sweep is complete).
+        // Space is recycled in record order (empty barriers); records are
+        // pulled into L2 PS_PF ahead so the copies are short.
+        const uint64_t pol = policy_evict_first();
+        uint32_t dhead = 0;
+        int oldest = 0;   // first record not yet known consumed
+        int issued = 0;
+        bool up_ready = false;
+        // record descriptors in registers, two windows of 32 (lane l: record base + l)
+        uint64_t cur_off = 0, nxt_off = 0;
+        uint32_t cur_bytes = 0, cur_foot = 0, cur_pm = 0, nxt_bytes = 0, nxt_foot = 0, nxt_pm = 0;
+        uint32_t cur_nr = 0, nxt_nr = 0;
+        auto fetch = [&](int j, uint64_t &off, uint32_t &bytes, uint32_t &foot, uint32_t &pos0u, uint32_t &nr) {
+            const PRecInfo &ri = a.rec[r0 + j];
+            off = ri.off;
+            bytes = ri.bytes;
+            foot = ri.foot;
+            pos0u = uint32_t(ri.pos0) | (uint32_t(ri.level & 1) << 31);
+            nr = uint32_t(ri.nrows);
+        };
+        if (lane < nrec) fetch(lane, cur_off, cur_bytes, cur_foot, cur_pm, cur_nr);
+        if (32 + lane < nrec) fetch(32 + lane, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
+        for (int j = lane; j < PS_PF && j < nrec; j += 32) bulk_prefetch_l2(a.recs + cur_off, cur_bytes);
+        for (; issued < nrec; ++issued) {
+            if (issued > 0 && (issued & 31) == 0) {   // slide the window by 32 records
+                cur_off = nxt_off;
+                cur_bytes = nxt_bytes;
+                cur_foot = nxt_foot;
+                cur_pm = nxt_pm;
+                cur_nr = nxt_nr;
+                const int j = issued + 32 + lane;
+                if (j < nrec) fetch(j, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
+            }
+            const int jl = issued & 31;
+            const uint64_t off = __shfl_sync(0xffffffffu, cur_off, jl);
+            const uint32_t bytes = __shfl_sync(0xffffffffu, cur_bytes, jl);
+            const uint32_t foot = __shfl_sync(0xffffffffu, cur_foot, jl);
+            const uint32_t pm = __shfl_sync(0xffffffffu, cur_pm, jl);
+            const uint32_t nr = __shfl_sync(0xffffffffu, cur_nr, jl);
+            const bool up = pm >> 31;
+            const uint32_t pos0 = pm & 0x7fffffffu;
+            bool ok = true;
+            if (up && !up_ready) {
+                // y_u is written by this part's L sweep: wait for every L record
+                // (both compute groups) before the first U' input copy
+                for (; ok && oldest < issued; ++oldest)
+                    ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                up_ready = true;
+            }
+            // wait for a free ring slot and room for the footprint
+            int64_t at = -1;
+            while (ok) {
+                if (issued - oldest >= K) {
+                    ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                    ++oldest;
+                    continue;
+                }
+                const int live = issued - oldest;
+                at = ring_alloc(dhead, live ? slot_off[oldest % K] : 0, live, foot, a.data_bytes);
+                if (at >= 0) break;
+                ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                ++oldest;
+            }
+            if (!ok) break;
+            const int si = issued % K;
+            // pull a record PS_PF ahead into L2 (no shared memory)
+            const int pf = issued + PS_PF;
+            const int pj = pf - (issued & ~31);   // index into the two windows
+            const uint64_t pf_off = __shfl_sync(0xffffffffu, pj < 32 ? cur_off : nxt_off, pj & 31);
+            const uint32_t pf_bytes = __shfl_sync(0xffffffffu, pj < 32 ? cur_bytes : nxt_bytes, pj & 31);
+            if (lane == 0) {
+                slot_off[si] = uint32_t(at);
+                const uint32_t in_bytes = nr * uint32_t(VS * 8);
+                mbar_expect_tx(full_bar + si, bytes + in_bytes);
+                bulk_g2s(dring + at, a.recs + off, bytes, full_bar + si, pol);
+                bulk_g2s(dring + at + bytes, (up ? a.y_u : a.b_perm) + size_t(pos0) * VS, in_bytes, full_bar + si, pol);
+                if (pf < nrec && pj < 64) bulk_prefetch_l2(a.recs + pf_off, pf_bytes);
+                if (a.trace) a.trace[size_t(r0 + issued) * 8 + 0] = globaltimer();
+            }
+            __syncwarp();
+        }
+        // never leave the CTA with copies in flight into its shared memory
+        for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + g % K, uint32_t(g / K) & 1u);
+    } else if (warp > PS_NW) {
+        // ============ poll: dependencies outside the on-chip ring ==============
+        // warp p owns records p, p + NPOLL, ...; all its loads of a round are
+        // in flight before any tag is checked (one L2 round trip per round)
+        const int pw = warp - PS_NW - 1;
+        for (int i = pw; i < nrec; i += PS_NPOLL) {
+            const int s = i % K;
+            if (!mbar_wait_or_abort(full_bar + s, uint32_t(i / K) & 1u, &abort_flag, a)) break;
+            if (a.trace && lane == 0) a.trace[size_t(r0 + i) * 8 + 1] = globaltimer();
+            unsigned char *rec = dring + slot_off[s];
+            const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
+            const int nr = h.nrows, ng = h.nglob;
+            const int32_t *gpos = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr)) + nr + h.S * nr;
+            double *dst = reinterpret_cast<double *>(rec + h.in_off) + size_t(nr) * VS;   // deps, component-major
+            const double *vec = (h.flags & 1) ? a.x_t : a.y_t;
+            uint32_t pend = 0;
+            int32_t pos[EPL];
+#pragma unroll
+            for (int m = 0; m < EPL; ++m) {
+                const int e = lane + 32 * m;
+                pos[m] = e < ng ? gpos[e] : 0;
+                if (e < ng) pend |= 1u << m;
+            }
+            uint64_t t0 = 0;
+            uint32_t spins = 0;
+            bool dead = false;
+            while (__any_sync(0xffffffffu, pend)) {
+                double v[EPL][BS];
+#pragma unroll
+                for (int m = 0; m < EPL; ++m)
+                    if (pend & (1u << m)) ld_row<BS>(vec + size_t(pos[m]) * VS, v[m]);
+#pragma unroll
+                for (int m = 0; m < EPL; ++m)
+                    if (pend & (1u << m)) {
+                        uint32_t ok = 1;
+#pragma unroll
+                        for (int q = 0; q < BS; ++q) ok &= (tag_of(v[m][q]) == par);
+                        if (ok) {
+#pragma unroll
+                            for (int q = 0; q < BS; ++q) dst[size_t(q) * ng + lane + 32 * m] = untag(v[m][q]);
+                            pend &= ~(1u << m);
+                        }
+                    }
+                if (pend && ps_timed_out(t0, spins, a)) {
+                    abort_flag = 1;
+                    dead = true;
+                }
+                if (__any_sync(0xffffffffu, dead)) break;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (a.trace) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
+                mbar_arrive(dep_bar + s);
+            }
+            if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
+        }
+    } else {
+        // ========================= compute warps ==============================
+        // two groups of PS_NG threads take alternate records (ping-pong).  A
+        // group prepares its next record while the other group computes:
+        // header, the row's accumulator init (b, or D^-1 y), its first SR
+        // blocks and the shared-memory addresses of their dependencies.  The
+        // hand-over is a named-barrier arrive/sync, so the level chain only
+        // carries [dependency loads -> products -> publish].
+        constexpr int SR = BS <= 2 ? 6 : (BS <= 3 ? 3 : (BS <= 4 ? 2 : 1));
+        const int grp = warp / (PS_NG / 32), gt = tid % PS_NG;
+        const uint32_t vring_s = smem_addr(vring);
+        for (int i = grp; i < nrec; i += 2) {
+            const int s = i % K;
+            const uint32_t ph = uint32_t(i / K) & 1u;
+            if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) break;
+            const unsigned char *rec = dring + slot_off[s];
+            const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
+            const int nr = h.nrows, S = h.S, ng = h.nglob;
+            const bool up = h.flags & 1;
+            const bool live = gt < nr;
+            const int32_t *iarr = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr));
+            const int32_t *desc = iarr + nr;
+            const double *vals = reinterpret_cast<const double *>(rec + h.vals_off) + gt + (up ? size_t(BS2) * nr : 0);
+            const double *inp = reinterpret_cast<const double *>(rec + h.in_off) + size_t(gt) * VS;
+            const uint32_t dep_s = smem_addr(rec + h.in_off) + uint32_t(nr * VS * 8);
+            double acc[BS];
+            double v[SR][BS2];
+            uint32_t xa[SR];   // shared address of component 0 of each staged dependency
+            uint32_t xs[SR];   // its component stride in bytes
+            int idx = 0;       // L: the row's U' position; U': its natural row
+            if (live) {
+                idx = iarr[gt];
+                if (up) {   // acc = D^-1 y: y is this part's own L result (no chain)
+                    const double *dv = vals - size_t(BS2) * nr;
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) {
+                        double z = dv[size_t(r) * nr] * inp[0];
+#pragma unroll
+                        for (int c = 1; c < BS; ++c) z = fma(dv[size_t(c * BS + r) * nr], inp[c], z);
+                        acc[r] = z;
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] = inp[r];
+                }
+#pragma unroll
+                for (int u = 0; u < SR; ++u) {
+                    const int32_t d = u < S ? desc[u * nr + gt] : a.ring_mask + 1;
+                    xa[u] = d >= 0 ? vring_s + uint32_t(d) * 8u : dep_s + uint32_t(-d - 1) * 8u;
+                    xs[u] = d >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
+#pragma unroll
+                    for (int e = 0; e < BS2; ++e) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
+                }
+            }
+            if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
+            if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 4] = globaltimer();
+            // the other group has published record i-1
+            if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);
+            if (live) {
+                // register-staged slots: every dependency load first, then the
+                // products, summed as a tree and subtracted once
+                double x[SR][BS];
+#pragma unroll
+                for (int u = 0; u < SR; ++u)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) x[u][c] = lds_f64(xa[u] + uint32_t(c) * xs[u]);
+                double pr[SR][BS];
+#pragma unroll
+                for (int u = 0; u < SR; ++u) {
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) pr[u][r] = v[u][r] * x[u][0];
+#pragma unroll
+                    for (int c = 1; c < BS; ++c)
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) pr[u][r] = fma(v[u][c * BS + r], x[u][c], pr[u][r]);
+                }
+#pragma unroll
+                for (int w = 1; w < SR; w <<= 1)
+#pragma unroll
+                    for (int u = 0; u + w < SR; u += 2 * w)
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) pr[u][r] += pr[u + w][r];
+#pragma unroll
+                for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
+                // remaining slots straight from shared memory
+                if (S > SR) {
+#pragma unroll 2
+                    for (int sl = SR; sl < S; ++sl) {
+                        const int32_t dd = desc[sl * nr + gt];
+                        const uint32_t ad = dd >= 0 ? vring_s + uint32_t(dd) * 8u : dep_s + uint32_t(-dd - 1) * 8u;
+                        const uint32_t st = dd >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
+                        double xv[BS];
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) xv[c] = lds_f64(ad + uint32_t(c) * st);
+                        const double *vv = vals + size_t(sl) * BS2 * nr;
+                        double p2[BS];
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) p2[r] = vv[size_t(r) * nr] * xv[0];
+#pragma unroll
+                        for (int c = 1; c < BS; ++c)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r) p2[r] = fma(vv[size_t(c * BS + r) * nr], xv[c], p2[r]);
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) acc[r] -= p2[r];
+                    }
+                }
+                // publish: ring (this part), tagged global vector (other parts),
+                // and y for this part's U' sweep (L) / the caller's x (U')
+                const uint32_t rs = vring_s + uint32_t((h.seq0 + gt) & a.ring_mask) * 8u;
+#pragma unroll
+                for (int r = 0; r < BS; ++r) sts_f64(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
+                double pub[BS];
+#pragma unroll
+                for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
+                st_row<BS>((up ? a.x_t : a.y_t) + size_t(h.pos0 + gt) * VS, pub);
+                if (up) {
+                    if (a.out) {
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) a.out[size_t(idx) * BS + r] = acc[r];
+                    }
+                } else {
+                    double *yu = a.y_u + size_t(idx) * VS;
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) yu[r] = acc[r];
+                }
+            }
+            // hand record i+1 to the other group, release record i's ring space
+            // (an L record's y_u stores are read later by the async proxy)
+            if (i + 1 < nrec) named_bar_arrive(1 + (grp ^ 1), 2 * PS_NG);
+            if (!up) fence_proxy_async_global();
+            mbar_arrive(empty_bar + s);
+            if (a.trace && gt == 0) {
+                a.trace[size_t(r0 + i) * 8 + 5] = globaltimer();
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                a.trace[size_t(r0 + i) * 8 + 6] = (uint64_t(blockIdx.x) << 32) | smid;
+                a.trace[size_t(r0 + i) * 8 + 7] = uint64_t(uint32_t(h.flags));
+            }
+        }
+    }
+    // the last CTA to finish advances the epoch (every CTA read it at entry)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last_cta = atomicAdd(&a.st->done_ctas, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_cta && tid == 0) {
+        __threadfence();
+        a.st->done_ctas = 0;
+        __threadfence();
+        atomicAdd(&a.st->epoch, 1u);
+    }
+}
+
+// b in L-position order (the L records' input bulk copies read it)
+template <int BS>
+__global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ posl, const double *__restrict__ b,
+                                 double *__restrict__ bp) {
+    constexpr int VS = ps_vec_stride(BS);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double v[VS];
+#pragma unroll
+        for (int c = 0; c < VS; ++c) v[c] = c < BS ? __ldg(b + i * BS + c) : 0.0;
+        double *d = bp + size_t(__ldg(posl + i)) * VS;
+        if constexpr (VS == 4) {
+            reinterpret_cast<double4 *>(d)[0] = make_double4(v[0], v[1], v[2], v[3]);
+        } else if constexpr (VS == 2) {
+            reinterpret_cast<double2 *>(d)[0] = make_double2(v[0], v[1]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < VS; ++c) d[c] = v[c];
+        }
+    }
+}
+
+// ===========================================================================
+// pack: scatter the index sections and fill the value areas of every record
+// from the factored P' values (L blocks verbatim, U' = D^-1 U after the split)
+// and D^-1; one warp per record.
+// ===========================================================================
+template <int BS>
+__global__ void ppack_kernel(int64_t nrec, const PRecInfo *__restrict__ info, const int32_t *__restrict__ idx,
+                             const int32_t *__restrict__ vmap, unsigned char *__restrict__ recs,
+                             const double *__restrict__ pvals, const double *__restrict__ dinv) {
+    constexpr int BS2 = BS * BS;
+    const int lane = threadIdx.x & 31;
+    const int64_t W = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nrec; r += W) {
+        const PRecInfo ri = info[r];
+        int32_t *dst = reinterpret_cast<int32_t *>(recs + ri.off);
+        const int32_t *src = idx + ri.idx_off;
+        for (uint32_t w = lane; w < ri.idx_words; w += 32) dst[w] = src[w];
+        const PRecHdr h = *reinterpret_cast<const PRecHdr *>(src);
+        const int nr = ri.nrows;
+        double *vals = reinterpret_cast<double *>(recs + ri.off + h.vals_off);
+        if ((h.flags & 1)) {
+            const int32_t *rows = src + sizeof(PRecHdr) / 4;
+            for (int e = lane; e < BS2 * nr; e += 32) {
+                const int el = e / nr, q = e - el * nr;
+                vals[e] = dinv[int64_t(rows[q]) * BS2 + el];
+            }
+            vals += int64_t(BS2) * nr;
+        }
+        const int64_t tot = int64_t(ri.S) * BS2 * nr;
+        for (int64_t e = lane; e < tot; e += 32) {
+            const int64_t sl = e / (int64_t(BS2) * nr);
+            const int rem = int(e - sl * BS2 * nr);
+            const int el = rem / nr, q = rem - el * nr;
+            const int32_t slot = vmap[ri.vmap_off + sl * nr + q];
+            vals[e] = slot >= 0 ? pvals[int64_t(slot) * BS2 + el] : 0.0;
+        }
+        // padding bytes between the index section and the values stay as
+        // cudaMalloc left them: they are never read
+    }
+}
+
+#define BILUK_BS_DISPATCH(bs, F)  \
+    switch (bs) {                 \
+        case 1: F(1); break;      \
+        case 2: F(2); break;      \
+        case 3: F(3); break;      \
+        case 4: F(4); break;      \
+        case 5: F(5); break;      \
+        case 6: F(6); break;      \
+        case 7: F(7); break;      \
+        case 8: F(8); break;      \
+        default: return cudaErrorInvalidValue; \
+    }
+
+size_t psweep_smem_bytes(const Plan &p) {
+    const PSweep &ps = p.ps;
+    return size_t(ps.ring + 2) * ps_vec_stride(p.bs) * 8 + size_t(ps.xval_ring) + size_t(ps.data_ring);
+}
+
+cudaError_t launch_ppack(const Plan &p, cudaStream_t s) {
+    const PSweep &ps = p.ps;
+    const int64_t nrec = int64_t(ps.rec.size());
+    if (nrec == 0) return cudaSuccess;
+    const PRecInfo *info = reinterpret_cast<const PRecInfo *>(p.ws + p.off.ps_info);
+    const int32_t *idx = reinterpret_cast<const int32_t *>(p.ws + p.off.ps_idx);
+    const int32_t *vmap = reinterpret_cast<const int32_t *>(p.ws + p.off.ps_vmap);
+    unsigned char *recs = p.ws + p.off.ps_rec;
+    const double *pv = reinterpret_cast<const double *>(p.ws + p.off.pvals);
+    const double *dv = reinterpret_cast<const double *>(p.ws + p.off.dinv);
+    int64_t grid = (nrec + 7) / 8;
+    if (grid > int64_t(p.num_sms) * 64) grid = int64_t(p.num_sms) * 64;
+#define PPACK_LAUNCH(BS) ppack_kernel<BS><<<unsigned(grid), 256, 0, s>>>(nrec, info, idx, vmap, recs, pv, dv);
+    BILUK_BS_DISPATCH(p.bs, PPACK_LAUNCH)
+#undef PPACK_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s) {
+    const int32_t *posl = reinterpret_cast<const int32_t *>(p.ws + p.off.ps_posl);
+    double *bp = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
+    int64_t grid = (p.n + 255) / 256;
+    if (grid > int64_t(p.num_sms) * 16) grid = int64_t(p.num_sms) * 16;
+    if (grid < 1) grid = 1;
+#define PERM_LAUNCH(BS) permute_b_kernel<BS><<<unsigned(grid), 256, 0, s>>>(p.n, posl, b, bp);
+    BILUK_BS_DISPATCH(p.bs, PERM_LAUNCH)
+#undef PERM_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s) {
+    const size_t smem = psweep_smem_bytes(p);
+    dim3 grid(p.ps.P), block(PS_NT + 32 * PS_NAUX);
+#define PSWEEP_LAUNCH(BS)                                                                                  \
+    {                                                                                                      \
+        auto kern = psweep_kernel<BS>;                                                                     \
+        cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+        if (e0 != cudaSuccess) return e0;                                                                  \
+        void *args[] = {const_cast<PSweepArgs *>(&a)};                                                     \
+        e0 = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), grid, block, args, smem, s); \
+        if (e0 != cudaSuccess) return e0;                                                                  \
+    }
+    BILUK_BS_DISPATCH(p.bs, PSWEEP_LAUNCH)
+#undef PSWEEP_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm) {
+    const size_t smem = psweep_smem_bytes(p);
+#define POCC(BS)                                                                                                  \
+    {                                                                                                             \
+        auto kern = psweep_kernel<BS>;                                                                            \
+        cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));      \
+        if (e0 != cudaSuccess) return e0;                                                                         \
+        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, PS_NT + 32 * PS_NAUX, smem);                \
+        if (e0 != cudaSuccess) return e0;                                                                         \
+    }
+    BILUK_BS_DISPATCH(p.bs, POCC)
+#undef POCC
+    return cudaSuccess;
+}
+
+}  // namespace biluk

@@ -1,0 +1,440 @@
+// Host planner of the partitioned sweep (the apply engine).
+//
+// Replaces the execution side of build_level_schedule / _pack_level
+// (trisolve.py:83-118): the reference packs every level of each triangle
+// into one gather/reduceat/scatter pass per level (trisolve.py:121-145); here
+// the same level sets (global block levels of L and U', bit-exact with
+// level_schedule) order the rows INSIDE contiguous row ranges ("parts"), one
+// CTA per part, and the records a CTA streams are laid out back to back.
+// Integer work only; the values are packed on the device (ppack_kernel).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "biluk_internal.h"
+
+namespace biluk {
+
+namespace {
+
+inline int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+// bytes of a record with the given shape (layout: biluk_internal.h)
+inline int64_t rec_index_words(int nrows, int S, int nglob, bool upper) {
+    (void)upper;
+    return int64_t(sizeof(PRecHdr) / 4) + int64_t(nrows) + int64_t(S) * nrows + nglob;
+}
+inline int64_t rec_vals_off(int nrows, int S, int nglob, bool upper) {
+    return a16(4 * rec_index_words(nrows, S, nglob, upper));
+}
+inline int64_t rec_total_bytes(int bs2, int nrows, int S, int nglob, bool upper) {
+    return a16(rec_vals_off(nrows, S, nglob, upper) + 8 * int64_t(bs2) * nrows * (S + (upper ? 1 : 0)));
+}
+// shared-memory footprint: the streamed bytes, the inputs (vs doubles per
+// row) and the fetched dependencies (bs doubles each)
+inline int64_t rec_foot_bytes(int bs2, int vs, int nrows, int S, int nglob, bool upper) {
+    const int bs = int(std::lround(std::sqrt(double(bs2))));
+    return rec_total_bytes(bs2, nrows, S, nglob, upper) + int64_t(nrows) * vs * 8 + a16(int64_t(nglob) * bs * 8);
+}
+
+inline int32_t nslot_of(const Plan &p, int64_t i, bool upper) {
+    return upper ? p.p_rp[i + 1] - p.p_diag[i] - 1 : p.p_diag[i] - p.p_rp[i];
+}
+inline int32_t first_slot_of(const Plan &p, int64_t i, bool upper) { return upper ? p.p_diag[i] + 1 : p.p_rp[i]; }
+
+// streamed bytes of row i in both sweeps (balancing weight)
+inline int64_t row_weight(const Plan &p, int64_t i) {
+    const int64_t s = nslot_of(p, i, false) + nslot_of(p, i, true), bs2 = int64_t(p.bs) * p.bs;
+    return (s + 1) * bs2 * 8 + 8 * s + 16 * p.bs + 16;
+}
+
+// contiguous row ranges of (nearly) equal streamed bytes
+void partition_contiguous(const Plan &p, int P, Partition &pt) {
+    const int64_t n = p.n;
+    std::vector<int64_t> cum(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) cum[i + 1] = cum[i] + row_weight(p, i);
+    std::vector<int32_t> ptr(P + 1, 0);
+    ptr[P] = int32_t(n);
+    for (int c = 1; c < P; ++c) {
+        const int64_t target = (cum[n] * c + P / 2) / P;
+        int64_t r = std::lower_bound(cum.begin(), cum.end(), target) - cum.begin();
+        r = std::max<int64_t>(r, ptr[c - 1]);
+        ptr[c] = int32_t(std::min<int64_t>(r, n));
+    }
+    pt.P = P;
+    pt.kind = 0;
+    pt.part_of.resize(n);
+    for (int c = 0; c < P; ++c)
+        for (int32_t i = ptr[c]; i < ptr[c + 1]; ++i) pt.part_of[i] = c;
+}
+
+// structured-grid columns: (y, z) blocks spanning every x of a natural-order grid
+void partition_columns(const Plan &p, int P, const int64_t g[3], Partition &pt) {
+    const int64_t nx = g[0], ny = g[1], nz = g[2];
+    int best_y = 1, best_z = 1;
+    double best = -1e300;
+    for (int pz = 1; pz <= std::min<int64_t>(P, nz); ++pz) {
+        const int py = int(std::min<int64_t>(ny, P / pz));
+        if (py < 1) continue;
+        const double score = double(py) * pz - 1.0 * (py + pz);   // count, then short hop chains
+        if (score > best) {
+            best = score;
+            best_y = py;
+            best_z = pz;
+        }
+    }
+    pt.P = best_y * best_z;
+    pt.kind = 1;
+    pt.grid[0] = nx;
+    pt.grid[1] = ny;
+    pt.grid[2] = nz;
+    pt.split[0] = best_y;
+    pt.split[1] = best_z;
+    pt.part_of.resize(p.n);
+    for (int64_t k = 0; k < nz; ++k) {
+        const int cz = int(k * best_z / nz);
+        for (int64_t j = 0; j < ny; ++j) {
+            const int c = cz * best_y + int(j * best_y / ny);
+            const int64_t r = (k * ny + j) * nx;
+            for (int64_t i = 0; i < nx; ++i) pt.part_of[r + i] = c;
+        }
+    }
+}
+
+// rows of every part (ascending) and their position bases
+void partition_finish(Partition &pt) {
+    pt.rows.assign(pt.P, {});
+    std::vector<int64_t> cnt(pt.P, 0);
+    for (int32_t c : pt.part_of) cnt[c]++;
+    for (int c = 0; c < pt.P; ++c) pt.rows[c].reserve(cnt[c]);
+    for (size_t i = 0; i < pt.part_of.size(); ++i) pt.rows[pt.part_of[i]].push_back(int32_t(i));
+    pt.base.assign(pt.P + 1, 0);
+    for (int c = 0; c < pt.P; ++c) pt.base[c + 1] = pt.base[c] + int32_t(cnt[c]);
+}
+
+// a part's rows in (level, row) order
+void part_order(const std::vector<int32_t> &lev, const std::vector<int32_t> &rows, std::vector<int32_t> &ord) {
+    ord = rows;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return lev[a] < lev[b]; });
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Natural-order structured grid (nx, ny, nz) behind the block pattern of A, if
+// any: the offsets 1, nx and nx*ny must each occur in >= n/4 rows.  Only the
+// partition's QUALITY depends on this guess -- any row -> part assignment is
+// correct, because every CTA walks its rows in global level order.
+// ---------------------------------------------------------------------------
+bool detect_grid(const Plan &p, int64_t g[3]) {
+    const int64_t n = p.n;
+    if (n < 8) return false;
+    std::vector<int64_t> offs;
+    offs.reserve(size_t(p.nnzA));
+    for (int64_t i = 0; i < n; ++i)
+        for (int32_t t = p.a_rp[i]; t < p.a_rp[i + 1]; ++t)
+            if (p.a_ci[t] > i) offs.push_back(p.a_ci[t] - i);
+    std::sort(offs.begin(), offs.end());
+    std::vector<std::pair<int64_t, int64_t>> freq;   // offset, count
+    for (size_t a = 0; a < offs.size();) {
+        size_t b = a;
+        while (b < offs.size() && offs[b] == offs[a]) ++b;
+        if (int64_t(b - a) * 4 >= n) freq.emplace_back(offs[a], int64_t(b - a));
+        a = b;
+    }
+    auto has = [&](int64_t o) {
+        for (auto &f : freq)
+            if (f.first == o) return true;
+        return false;
+    };
+    if (!has(1)) return false;
+    for (auto &fx : freq) {
+        const int64_t nx = fx.first;
+        if (nx < 2 || n % nx) continue;
+        for (auto it = freq.rbegin(); it != freq.rend(); ++it) {
+            const int64_t nxy = it->first;
+            if (nxy <= nx || nxy % nx || n % nxy) continue;
+            g[0] = nx;
+            g[1] = nxy / nx;
+            g[2] = n / nxy;
+            return true;
+        }
+        // a 2-D grid: nx and n / nx
+        g[0] = nx;
+        g[1] = n / nx;
+        g[2] = 1;
+        return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// Cost model used to choose the partition: a level-group-granular simulation
+// of the sweeps.  A level group of a part starts when the part's previous
+// group is done and every cross-part dependency has been published + HOP; it
+// takes TAU per record plus its streamed bytes at the per-SM rate.  The apply
+// is at least the streamed bytes over the HBM rate.
+// ---------------------------------------------------------------------------
+double psweep_estimate_us(const Plan &p, const Partition &pt) {
+    const double HOP = 1.0, TAU = 0.45, BW_SM = 80e3, BW_HBM = 6.0e6;   // us, bytes/us
+    const int64_t n = p.n, bs2 = int64_t(p.bs) * p.bs;
+    if (n == 0) return 0.0;
+    const int P = pt.P;
+    std::vector<double> finL(n, 0.0), finU(n, 0.0), part_l_end(P, 0.0);
+    std::vector<int32_t> ord;
+    double total_bytes = 0;
+    double end = 0;
+    // parts in an order in which every cross-part dependency is already timed:
+    // L by the smallest row, U' by the largest (a part's rows may interleave
+    // with others' -- fall back to sweeping the rows in level order globally)
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool up = pass == 1;
+        const std::vector<int32_t> &lev = up ? p.lev_U : p.lev_L;
+        std::vector<double> &fin = up ? finU : finL;
+        const int32_t nlev = up ? p.nlev_U : p.nlev_L;
+        // rows bucketed by level; within a level, per part: group start/end
+        std::vector<std::vector<int32_t>> bylev(nlev + 1);
+        for (int64_t i = 0; i < n; ++i) bylev[lev[i]].push_back(int32_t(i));
+        std::vector<double> t(P, 0.0);
+        for (int c = 0; c < P; ++c) t[c] = up ? part_l_end[c] : 0.0;
+        std::vector<double> ready(P), bytes(P);
+        std::vector<int32_t> rows_in(P, 0);
+        for (int32_t l = 1; l <= nlev; ++l) {
+            for (int32_t i : bylev[l]) {
+                const int c = pt.part_of[i];
+                if (rows_in[c] == 0) {
+                    ready[c] = t[c];
+                    bytes[c] = 0;
+                }
+                rows_in[c]++;
+                const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                for (int32_t s = fs; s < fs + ns; ++s) {
+                    const int32_t j = p.p_ci[s];
+                    if (pt.part_of[j] != c) ready[c] = std::max(ready[c], fin[j] + HOP);
+                }
+                bytes[c] += double(ns + (up ? 1 : 0)) * bs2 * 8 + 4 * ns + 16 * p.bs;
+            }
+            for (int32_t i : bylev[l]) {
+                const int c = pt.part_of[i];
+                if (rows_in[c] > 0) {
+                    const double recs = std::ceil(double(rows_in[c]) / 128.0);
+                    t[c] = ready[c] + recs * TAU + bytes[c] / BW_SM;
+                    total_bytes += bytes[c];
+                    rows_in[c] = 0;
+                }
+                fin[i] = t[c];
+            }
+        }
+        for (int c = 0; c < P; ++c) {
+            if (!up) part_l_end[c] = t[c];
+            end = std::max(end, t[c]);
+        }
+    }
+    return std::max(end, total_bytes / BW_HBM);
+}
+
+// ---------------------------------------------------------------------------
+// Build the records of both sweeps for P parts.
+// ---------------------------------------------------------------------------
+int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
+    PSweep &ps = p.ps;
+    const int bs = p.bs, bs2 = bs * bs, vs = ps_vec_stride(bs);
+    const int64_t n = p.n;
+    // ---- choose the partition ---------------------------------------------------
+    // structured grids: (y, z) columns; anything else: contiguous row ranges.
+    // P: every SM for large systems, else the cost model's choice.
+    int64_t g[3] = {0, 0, 0};
+    bool grid = detect_grid(p, g);
+    if (const char *env = std::getenv("BILUK_PARTITION")) grid = grid && std::string(env) != "contiguous";
+    int P = parts;
+    if (const char *env = std::getenv("BILUK_PARTS")) P = std::atoi(env);
+    Partition pt;
+    auto make = [&](int cand, Partition &out) {
+        cand = int(std::max<int64_t>(1, std::min<int64_t>(cand, std::max<int64_t>(1, n))));
+        if (grid)
+            partition_columns(p, cand, g, out);
+        else
+            partition_contiguous(p, cand, out);
+        partition_finish(out);
+    };
+    ps.est_us = 0;
+    if (P > 0 || n >= int64_t(num_sms) * 4096) {
+        make(P > 0 ? std::min(P, num_sms) : num_sms, pt);
+    } else {
+        double best = 1e300;
+        for (int cand = num_sms; cand >= 1; cand /= 2) {
+            Partition c;
+            make(cand, c);
+            const double e = psweep_estimate_us(p, c);
+            if (e < best * 0.97) {
+                best = e;
+                pt = std::move(c);
+            }
+        }
+        ps.est_us = best;
+    }
+    P = pt.P;
+    ps.P = P;
+    ps.partition = pt.kind;
+    for (int d = 0; d < 3; ++d) ps.grid[d] = pt.grid[d];
+    ps.split[0] = pt.split[0];
+    ps.split[1] = pt.split[1];
+    // ---- shared-memory budget of one CTA ---------------------------------------
+    ps.nthreads = 128;
+    ps.ring = bs <= 4 ? 512 : 256;
+    const int64_t vring = int64_t(ps.ring + 2) * vs * 8;
+    ps.xval_ring = 0;   // fetched values live in each record's footprint
+    const int64_t budget = int64_t(smem_per_block) - 2048;   // static shared + barriers
+    ps.data_ring = ((budget - vring - ps.xval_ring) / 1024) * 1024;
+    if (ps.data_ring < 16 * 1024) return fail(BILUK_EUNSUPPORTED, "not enough shared memory for the sweep");
+    ps.rec_cap = std::min<int64_t>(ps.data_ring / 4, 48 * 1024);
+    ps.glob_cap = PS_GLOB_CAP;
+
+    ps.posL.assign(n, -1);
+    ps.posU.assign(n, -1);
+    std::vector<std::vector<int32_t>> ordL(P), ordU(P);
+    for (int c = 0; c < P; ++c) {
+        part_order(p.lev_L, pt.rows[c], ordL[c]);
+        part_order(p.lev_U, pt.rows[c], ordU[c]);
+        for (size_t q = 0; q < ordL[c].size(); ++q) ps.posL[ordL[c][q]] = int32_t(pt.base[c] + q);
+        for (size_t q = 0; q < ordU[c].size(); ++q) ps.posU[ordU[c][q]] = int32_t(pt.base[c] + q);
+    }
+
+    ps.rec.clear();
+    ps.idx.clear();
+    ps.vmap.clear();
+    ps.part_rec.assign(P + 1, 0);
+    ps.rec_total = ps.max_rec = ps.max_glob = ps.nglob_total = 0;
+    ps.nlrec_max = 0;
+    const int32_t mask = ps.ring - 1;
+    std::vector<int32_t> gl;     // a record's deduplicated dependency positions
+    std::vector<int32_t> nfar;   // per row of a level group: dependencies outside the ring
+    for (int c = 0; c < P; ++c) {
+        ps.part_rec[c] = int32_t(ps.rec.size());
+        const int32_t b0 = pt.base[c];
+        const int32_t m = pt.base[c + 1] - b0;
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool up = pass == 1;
+            const std::vector<int32_t> &ord = up ? ordU[c] : ordL[c];
+            const std::vector<int32_t> &lev = up ? p.lev_U : p.lev_L;
+            const std::vector<int32_t> &pos = up ? ps.posU : ps.posL;
+            const int32_t seq_base = up ? m : 0;   // ring sequence continues from the L sweep
+            const size_t rec_begin = ps.rec.size();
+            size_t g0 = 0;
+            while (g0 < ord.size()) {
+                size_t ge = g0;
+                while (ge < ord.size() && lev[ord[ge]] == lev[ord[g0]]) ++ge;
+                const int64_t lvl_end_seq = seq_base + int64_t(ge);
+                // a dependency j of a row of this level is on chip iff it is in this part
+                // and the level's own writes cannot have recycled its ring slot
+                auto in_ring = [&](int32_t j) {
+                    return pt.part_of[j] == c && seq_base + int64_t(pos[j] - b0) >= lvl_end_seq - ps.ring;
+                };
+                nfar.assign(ge - g0, 0);
+                for (size_t q = g0; q < ge; ++q) {
+                    const int32_t i = ord[q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int32_t s = fs; s < fs + ns; ++s) nfar[q - g0] += in_ring(p.p_ci[s]) ? 0 : 1;
+                }
+                size_t a = g0;
+                while (a < ge) {
+                    // greedy record: rows, footprint and fetched dependencies under their caps
+                    size_t e = a;
+                    int S = 0;
+                    int64_t far = 0;
+                    while (e < ge && int64_t(e - a) < ps.nthreads) {
+                        const int32_t i = ord[e];
+                        const int S2 = std::max<int>(S, nslot_of(p, i, up));
+                        const int64_t far2 = far + nfar[e - g0];
+                        const int nr = int(e - a + 1);
+                        if (e > a && (rec_foot_bytes(bs2, vs, nr, S2, int(far2), up) > ps.rec_cap || far2 > ps.glob_cap))
+                            break;
+                        S = S2;
+                        far = far2;
+                        ++e;
+                    }
+                    const int nr = int(e - a);
+                    gl.clear();
+                    for (size_t q = a; q < e; ++q) {
+                        const int32_t i = ord[q];
+                        const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                        for (int32_t s = fs; s < fs + ns; ++s)
+                            if (!in_ring(p.p_ci[s])) gl.push_back(pos[p.p_ci[s]]);
+                    }
+                    std::sort(gl.begin(), gl.end());
+                    gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+                    const int nglob = int(gl.size());
+                    const int64_t foot = rec_foot_bytes(bs2, vs, nr, S, nglob, up);
+                    if (nglob > ps.glob_cap || foot > ps.data_ring / 2 || foot >= (int64_t(1) << 31))
+                        return fail(BILUK_EUNSUPPORTED, "a block row is too long for the partitioned sweep");
+                    PRecInfo info{};
+                    info.nrows = nr;
+                    info.S = S;
+                    info.level = lev[ord[a]] * 2 + (up ? 1 : 0);
+                    info.nglob = nglob;
+                    info.pos0 = int32_t(b0 + int32_t(a));
+                    info.bytes = uint32_t(rec_total_bytes(bs2, nr, S, nglob, up));
+                    info.foot = uint32_t(foot);
+                    info.idx_words = uint32_t(rec_index_words(nr, S, nglob, up));
+                    info.off = uint64_t(ps.rec_total);
+                    info.idx_off = uint64_t(ps.idx.size());
+                    info.vmap_off = int64_t(ps.vmap.size());
+                    ps.rec_total += info.bytes;
+                    ps.max_rec = std::max<int64_t>(ps.max_rec, foot);
+                    ps.max_glob = std::max<int64_t>(ps.max_glob, nglob);
+                    ps.nglob_total += nglob;
+                    PRecHdr h{};
+                    h.nrows = nr;
+                    h.S = S;
+                    h.nglob = nglob;
+                    h.flags = lev[ord[a]] * 2 + (up ? 1 : 0);
+                    h.seq0 = int32_t(seq_base + int32_t(a));
+                    h.pos0 = int32_t(b0 + int32_t(a));
+                    h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
+                    h.in_off = int32_t(info.bytes);
+                    const size_t base = ps.idx.size();
+                    ps.idx.resize(base + size_t(a16(4 * int64_t(info.idx_words)) / 4), 0);   // 16-byte aligned sections
+                    std::memcpy(ps.idx.data() + base, &h, sizeof(h));
+                    int32_t *w = ps.idx.data() + base + sizeof(PRecHdr) / 4;
+                    for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
+                    w += nr;
+                    int32_t *desc = w;
+                    int32_t *gpos = w + int64_t(S) * nr;
+                    for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
+                    const size_t vbase = ps.vmap.size();
+                    ps.vmap.resize(vbase + size_t(S) * nr, -1);
+                    for (int q = 0; q < nr; ++q) {
+                        const int32_t i = ord[a + q];
+                        const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                        for (int s = 0; s < S; ++s) {
+                            int32_t d = ps.ring;   // zero slot
+                            if (s < ns) {
+                                const int32_t j = p.p_ci[fs + s];
+                                if (in_ring(j)) {
+                                    d = int32_t((seq_base + int64_t(pos[j] - b0)) & mask);
+                                } else {
+                                    const int64_t at = std::lower_bound(gl.begin(), gl.end(), pos[j]) - gl.begin();
+                                    d = -int32_t(at) - 1;   // fetched dependency `at`
+                                }
+                                ps.vmap[vbase + size_t(s) * nr + q] = fs + s;
+                            }
+                            desc[int64_t(s) * nr + q] = d;
+                        }
+                    }
+                    ps.rec.push_back(info);
+                    a = e;
+                }
+                g0 = ge;
+            }
+            if (!up) ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
+        }
+    }
+    ps.part_rec[P] = int32_t(ps.rec.size());
+    if (ps.rec.size() >= size_t(INT32_MAX)) return fail(BILUK_EUNSUPPORTED, "too many sweep records");
+    return BILUK_OK;
+}
+
+}  // namespace biluk

@@ -32,7 +32,8 @@ __all__ = ["BlockIlukFactors", "build_preconditioner", "symbolic_phase"]
 
 _INFO_KEYS = ("n", "bs", "k", "nnzb_a", "nnzb_p", "nL", "nU", "levels_L", "levels_U", "tiles_L", "tiles_U",
               "rows_per_tile", "workspace_bytes", "apply_bytes", "spmv_bytes", "sweep_ctas", "sweep_warps",
-              "sweep_stages", "stage_bytes", "max_slots")
+              "sweep_stages", "stage_bytes", "max_slots", "engine", "parts", "records", "est_ns", "record_bytes",
+              "fetched_entries", "partition", "split_y", "split_z")
 
 
 def symbolic_phase(pattern, k):
@@ -120,7 +121,10 @@ class BlockIlukFactors:
         from .device import torch
         t = torch()
         inf = self.info
-        self._trace = t.zeros((inf["tiles_L"] + inf["tiles_U"], 4), dtype=t.int64, device="cuda")
+        if inf["engine"] == 1:   # partitioned sweep: 8 stamps per record (see csrc/psweep.cu)
+            self._trace = t.zeros((inf["records"] + 8192, 8), dtype=t.int64, device="cuda")
+        else:
+            self._trace = t.zeros((inf["tiles_L"] + inf["tiles_U"], 4), dtype=t.int64, device="cuda")
         nat.check(nat.lib().biluk_plan_set_trace(self._h, self._trace.data_ptr()))
         return self._trace
 
