@@ -125,6 +125,11 @@ int biluk_plan_set_trace(biluk_plan_t *plan, void *dev_trace);
  * tiles levels_L+1..), host array of info[9]+info[10] entries. */
 int biluk_plan_tile_levels(const biluk_plan_t *plan, int32_t *levels);
 
+/* Diagnostics: copies up to max_records sweep-record descriptors (64 bytes
+ * each, layout PRecInfo in csrc/biluk_internal.h) to `out` (may be NULL) and
+ * returns the number of records of the plan's partitioned sweep. */
+int biluk_plan_records(const biluk_plan_t *plan, void *out, int64_t max_records);
+
 /* Synchronises the stream and returns the sticky device status of the plan
  * (BILUK_OK or BILUK_ETIMEOUT), clearing it. */
 int biluk_plan_status(biluk_plan_t *plan, void *stream);

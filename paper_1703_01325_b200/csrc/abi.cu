@@ -305,6 +305,14 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     return BILUK_OK;
 }
 
+int biluk_plan_records(const biluk_plan_t *plan, void *out, int64_t max_records) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    const PSweep &ps = plan->p.ps;
+    const int64_t n = std::min<int64_t>(max_records, int64_t(ps.rec.size()));
+    if (out && n > 0) std::memcpy(out, ps.rec.data(), size_t(n) * sizeof(PRecInfo));
+    return int(std::min<int64_t>(int64_t(ps.rec.size()), INT32_MAX));
+}
+
 int biluk_plan_tile_levels(const biluk_plan_t *plan, int32_t *levels) {
     if (!plan) return fail(BILUK_EARG, "null plan");
     const Plan &p = plan->p;

@@ -122,7 +122,7 @@ class BlockIlukFactors:
         t = torch()
         inf = self.info
         if inf["engine"] == 1:   # partitioned sweep: 8 stamps per record (see csrc/psweep.cu)
-            self._trace = t.zeros((inf["records"] + 8192, 8), dtype=t.int64, device="cuda")
+            self._trace = t.zeros((inf["records"] + 16384, 8), dtype=t.int64, device="cuda")
         else:
             self._trace = t.zeros((inf["tiles_L"] + inf["tiles_U"], 4), dtype=t.int64, device="cuda")
         nat.check(nat.lib().biluk_plan_set_trace(self._h, self._trace.data_ptr()))
