@@ -133,8 +133,11 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     }
     // apply engine: the partitioned sweep; the tiled level-order sweep only
     // for patterns the partitioned one cannot stage (very long block rows)
+    // measured on B200 (tools/engine_compare.py): the
+    // partitioned sweep wins for ILU(0) with small blocks; with fill (longer
+    // rows, 2-4x the levels) or bs > 4 the tiled level-order sweep is faster
     Plan &P = h->p;
-    P.engine = 1;
+    P.engine = (k == 0 && bs <= 4) ? 1 : 0;
     if (const char *env = std::getenv("BILUK_ENGINE")) P.engine = std::atoi(env) == 0 ? 0 : 1;
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);

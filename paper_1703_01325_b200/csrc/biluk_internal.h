@@ -160,7 +160,8 @@ struct PRecInfo {       // 64 bytes: one per record, read by the producer, the g
 };
 // doubles per position of the partitioned sweep's vectors (>= 2: 16-byte rows)
 BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
-constexpr int PS_GLOB_CAP = 128;   // fetched dependencies per record (one per prefetch thread)
+// fetched dependencies per record (a multiple of 32: one per poll lane and round)
+BILUK_HD constexpr inline int ps_glob_cap(int bs) { return bs <= 4 ? 256 : 128; }
 constexpr int PS_KSLOTS = 16;      // records in flight per CTA (mbarrier sets)
 
 // an assignment of block rows to parts (any assignment is deadlock-free:

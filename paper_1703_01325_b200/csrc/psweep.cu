@@ -49,14 +49,6 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts_f64(uint32_t addr, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
 __device__ __forceinline__ void named_bar_arrive(int id, int threads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -146,7 +138,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
     constexpr int BS2 = BS * BS;
     constexpr int VS = ps_vec_stride(BS);
     constexpr int K = PS_KSLOTS;
-    constexpr int EPL = PS_GLOB_CAP / 32;   // dependency entries per poll lane
+    constexpr int EPL = ps_glob_cap(BS) / 32;   // dependency entries per poll lane
     static_assert(K % PS_NPOLL == 0, "poll warps must own whole ring slots");
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[K];    // record bytes + inputs landed (two bulk copies)
@@ -330,7 +322,12 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
         // carries [dependency loads -> products -> publish].
         constexpr int SR = BS <= 2 ? 6 : (BS <= 3 ? 3 : (BS <= 4 ? 2 : 1));
         const int grp = warp / (PS_NG / 32), gt = tid % PS_NG;
-        const uint32_t vring_s = smem_addr(vring);
+        // dependency addresses are byte offsets into the dynamic shared memory;
+        // plain C++ accesses let the compiler overlap the loads (they stay
+        // ordered against the barriers, which clobber memory)
+        const uint32_t vring_s = 0;   // the vector ring starts the dynamic shared memory
+        auto lds = [&](uint32_t off) -> double { return *reinterpret_cast<const double *>(smem + off); };
+        auto sts = [&](uint32_t off, double v) { *reinterpret_cast<double *>(smem + off) = v; };
         for (int i = grp; i < nrec; i += 2) {
             const int s = i % K;
             const uint32_t ph = uint32_t(i / K) & 1u;
@@ -344,7 +341,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             const int32_t *desc = iarr + nr;
             const double *vals = reinterpret_cast<const double *>(rec + h.vals_off) + gt + (up ? size_t(BS2) * nr : 0);
             const double *inp = reinterpret_cast<const double *>(rec + h.in_off) + size_t(gt) * VS;
-            const uint32_t dep_s = smem_addr(rec + h.in_off) + uint32_t(nr * VS * 8);
+            const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
             double acc[BS];
             double v[SR][BS2];
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
@@ -385,7 +382,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
 #pragma unroll
                 for (int u = 0; u < SR; ++u)
 #pragma unroll
-                    for (int c = 0; c < BS; ++c) x[u][c] = lds_f64(xa[u] + uint32_t(c) * xs[u]);
+                    for (int c = 0; c < BS; ++c) x[u][c] = lds(xa[u] + uint32_t(c) * xs[u]);
                 double pr[SR][BS];
 #pragma unroll
                 for (int u = 0; u < SR; ++u) {
@@ -404,33 +401,42 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                         for (int r = 0; r < BS; ++r) pr[u][r] += pr[u + w][r];
 #pragma unroll
                 for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
-                // remaining slots straight from shared memory
-                if (S > SR) {
-#pragma unroll 2
-                    for (int sl = SR; sl < S; ++sl) {
-                        const int32_t dd = desc[sl * nr + gt];
-                        const uint32_t ad = dd >= 0 ? vring_s + uint32_t(dd) * 8u : dep_s + uint32_t(-dd - 1) * 8u;
-                        const uint32_t st = dd >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
-                        double xv[BS];
+                // remaining slots straight from shared memory, 4 at a time:
+                // descriptors, dependencies and blocks loaded before the FMAs
+                for (int sl0 = SR; sl0 < S; sl0 += 4) {
+                    uint32_t ad[4], st[4];
 #pragma unroll
-                        for (int c = 0; c < BS; ++c) xv[c] = lds_f64(ad + uint32_t(c) * st);
-                        const double *vv = vals + size_t(sl) * BS2 * nr;
-                        double p2[BS];
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t dd = sl0 + u < S ? desc[(sl0 + u) * nr + gt] : a.ring_mask + 1;
+                        ad[u] = dd >= 0 ? vring_s + uint32_t(dd) * 8u : dep_s + uint32_t(-dd - 1) * 8u;
+                        st[u] = dd >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
+                    }
+                    double xv[4][BS];
 #pragma unroll
-                        for (int r = 0; r < BS; ++r) p2[r] = vv[size_t(r) * nr] * xv[0];
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) xv[u][c] = lds(ad[u] + uint32_t(c) * st[u]);
+                    double p2[4][BS];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double *vv = vals + size_t(sl0 + u) * BS2 * nr;
+                        const bool on = sl0 + u < S;
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) p2[u][r] = on ? vv[size_t(r) * nr] * xv[u][0] : 0.0;
 #pragma unroll
                         for (int c = 1; c < BS; ++c)
 #pragma unroll
-                            for (int r = 0; r < BS; ++r) p2[r] = fma(vv[size_t(c * BS + r) * nr], xv[c], p2[r]);
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) acc[r] -= p2[r];
+                            for (int r = 0; r < BS; ++r)
+                                if (on) p2[u][r] = fma(vv[size_t(c * BS + r) * nr], xv[u][c], p2[u][r]);
                     }
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] -= (p2[0][r] + p2[1][r]) + (p2[2][r] + p2[3][r]);
                 }
                 // publish: ring (this part), tagged global vector (other parts),
                 // and y for this part's U' sweep (L) / the caller's x (U')
                 const uint32_t rs = vring_s + uint32_t((h.seq0 + gt) & a.ring_mask) * 8u;
 #pragma unroll
-                for (int r = 0; r < BS; ++r) sts_f64(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
+                for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
                 double pub[BS];
 #pragma unroll
                 for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);

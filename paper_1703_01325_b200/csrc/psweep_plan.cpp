@@ -291,7 +291,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     ps.data_ring = ((budget - vring - ps.xval_ring) / 1024) * 1024;
     if (ps.data_ring < 16 * 1024) return fail(BILUK_EUNSUPPORTED, "not enough shared memory for the sweep");
     ps.rec_cap = std::min<int64_t>(ps.data_ring / 4, 48 * 1024);
-    ps.glob_cap = PS_GLOB_CAP;
+    ps.glob_cap = ps_glob_cap(bs);
 
     ps.posL.assign(n, -1);
     ps.posU.assign(n, -1);
