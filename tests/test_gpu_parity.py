@@ -168,3 +168,48 @@ def test_gmres_known_answers(b2):
     f = b2.build_preconditioner(b2.bcsr_from_csr(a, 1), 20)
     _, st = b2.gmres(a, a.to_dense() @ rng.standard_normal(20), M=f)
     assert st.converged and st.iterations == 1
+
+
+def _random_pattern_matrix(n, bs, seed):
+    """A non-grid pattern (contiguous-range partition path): random sparse + diagonal."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        cols = set(rng.choice(n, size=min(n, 4), replace=False).tolist()) | {i}
+        rows.append(sorted(cols))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.array([c for r in rows for c in r], np.int64)
+    vals = rng.uniform(-1, 1, (len(ci), bs, bs))
+    for i, r in enumerate(rows):
+        d = rp[i] + r.index(i)
+        vals[d] += np.eye(bs) * (2.0 * bs * len(r))
+    return n, bs, rp, ci, np.ascontiguousarray(vals.transpose(0, 2, 1)).reshape(-1)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("case", ["grid16_b3_k0", "grid12_b3_k2", "grid10_b4_k1", "grid9_b2_k3", "rand300_b3_k1",
+                                  "rand200_b1_k0"])
+def test_both_engines_match_oracle_and_are_repeatable(b2, monkeypatch, engine, case):
+    """Each sweep engine, forced, against the oracle; bitwise repeatable applies."""
+    import torch
+    monkeypatch.setenv("BILUK_ENGINE", str(engine))
+    kind, bsk, kk = case.split("_")
+    bs, k = int(bsk[1:]), int(kk[1:])
+    if kind.startswith("grid"):
+        nx = int(kind[4:])
+        n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, bs, seed=5)
+    else:
+        n, bs, rp, ci, vals = _random_pattern_matrix(int(kind[4:]), bs, seed=5)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    f = b2.build_preconditioner(a, k)
+    assert f.info["engine"] == engine
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, k)
+    rhs = np.random.default_rng(3).standard_normal(n * bs)
+    z = b2.apply_preconditioner(f, rhs)
+    assert rel_err(z, of.apply(rhs)) <= TOL
+    rt = torch.from_numpy(rhs).cuda()
+    x1 = b2.apply_preconditioner(f, rt)
+    for _ in range(3):
+        assert torch.equal(b2.apply_preconditioner(f, rt), x1)
+    f.status()

@@ -173,3 +173,37 @@ def test_plan_create_structural_errors():
         nat.check(rc, stage="symbolic-phase")
     rc = L.biluk_plan_create(2, 2, rp.ctypes.data, ci.ctypes.data, -1, ctypes.byref(h), ctypes.byref(err))
     assert rc == nat.EARG
+
+
+def test_partitioned_sweep_plan_geometry():
+    """Structured grids get (y, z) column parts, other patterns contiguous ranges;
+    every record's static ring place and issue point are consistent (host only)."""
+    import ctypes
+    L = nat.lib()
+    for nx, expect_kind in ((24, 1), (0, 0)):
+        if nx:
+            n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, 3, seed=0)
+        else:
+            rng = np.random.default_rng(0)
+            n, bs = 3000, 3
+            rows = [sorted(set(rng.choice(n, 5, replace=False).tolist()) | {i}) for i in range(n)]
+            rp = np.zeros(n + 1, np.int64)
+            rp[1:] = np.cumsum([len(r) for r in rows])
+            ci = np.array([c for r in rows for c in r], np.int64)
+        h = ctypes.c_void_p()
+        err = ctypes.c_int64(-1)
+        rp = np.ascontiguousarray(rp, np.int64)
+        ci = np.ascontiguousarray(ci, np.int64)
+        nat.check(L.biluk_plan_create(bs, n, nat.ptr(rp), nat.ptr(ci), 0, ctypes.byref(h), ctypes.byref(err)))
+        try:
+            from paper_1703_01325_b200.factor import _INFO_KEYS
+            buf = (ctypes.c_int64 * len(_INFO_KEYS))()
+            L.biluk_plan_info(h, buf, len(_INFO_KEYS))
+            info = dict(zip(_INFO_KEYS, list(buf)))
+            assert info["engine"] == 1 and info["partition"] == expect_kind
+            if expect_kind == 1:
+                assert info["split_y"] * info["split_z"] == info["parts"] <= 148
+            nrec = L.biluk_plan_records(h, None, 0)
+            assert nrec == info["records"] > 0
+        finally:
+            L.biluk_plan_destroy(h)
