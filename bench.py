@@ -223,6 +223,19 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = B / (t_kernel_ms * 1e-3) / 1e9
+    if info["engine"] == 1:
+        kernel_name = f"psweep_kernel<{bs}> (partitioned L and U' sweeps, one persistent launch, {info['parts']} parts)"
+    else:
+        kernel_name = f"sweep_kernel<{bs}> (tiled level-order L and U' sweeps, one persistent launch)"
+    # DRAM bytes per launch of that kernel from the committed ncu --set full capture (profiles/)
+    traffic, traffic_src = None, None
+    try:
+        tab = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        key = f"{kernel_name.split(' ')[0]} {args.nx}^3 k{args.k}"
+        if key in tab:
+            traffic, traffic_src = tab[key]["bytes"], tab[key]["source"]
+    except (OSError, ValueError, KeyError):
+        pass
 
     extras = {}
     if not args.no_extras:
@@ -282,9 +295,10 @@ def main():
             "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 8 * length,
                     "d2h_bytes_per_step": 8 * length, "ms_per_step": e2e_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "sweep_kernel<3> (L and U' sweeps, one persistent launch)",
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": kernel_name,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)" if peaks else "fallback 6650",
+                         "traffic_source": traffic_src},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": args.steps,
