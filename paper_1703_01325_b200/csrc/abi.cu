@@ -199,7 +199,13 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     CUDA_TRY(up(p.off.ps_part, p.ps.part_rec.data(), 4 * p.ps.part_rec.size()), "upload");
     CUDA_TRY(up(p.off.ps_idx, p.ps.idx.data(), 4 * p.ps.idx.size()), "upload");
     CUDA_TRY(up(p.off.ps_vmap, p.ps.vmap.data(), 4 * p.ps.vmap.size()), "upload");
-    if (p.engine == 1) CUDA_TRY(up(p.off.ps_posl, p.ps.posL.data(), 4 * p.ps.posL.size()), "upload");
+    if (p.engine == 1) {   // position -> row (the b permutation gathers)
+        std::vector<int32_t> lrow(p.ps.posL.size());
+        for (size_t i = 0; i < lrow.size(); ++i) lrow[size_t(p.ps.posL[i])] = int32_t(i);
+        CUDA_TRY(cudaMemcpyAsync(p.ws + p.off.ps_posl, lrow.data(), 4 * lrow.size(), cudaMemcpyHostToDevice, s),
+                 "upload");
+        CUDA_TRY(cudaStreamSynchronize(s), "upload sync");
+    }
     CUDA_TRY(up(p.off.pos_l, p.sl.pos.data(), 4 * p.sl.pos.size()), "upload");
     CUDA_TRY(up(p.off.pos_u, p.su.pos.data(), 4 * p.su.pos.size()), "upload");
     // parity-tagged vectors start at parity 0 everywhere; the first apply uses parity 1

@@ -344,7 +344,7 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.num_sms = num_sms;
     if (p.engine == 1) {
         p.sweep_ctas = p.ps.P;
-        p.sweep_warps = 2 * p.ps.nthreads / 32 + 4;   // two compute groups + producer, gather, 2 poll
+        p.sweep_warps = 2 * p.ps.nthreads / 32 + 4;   // two compute groups + 2 producers + 2 poll
         p.sweep_stages = PS_KSLOTS;
         p.stage_bytes = p.ps.max_rec;
     } else {
@@ -396,7 +396,7 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.ps_idx = take(4 * p.ps.idx.size());
     p.off.ps_vmap = take(4 * p.ps.vmap.size());
     const bool ps_on = p.engine == 1;
-    p.off.ps_posl = take(ps_on ? 4 * p.n : 0);                               // row -> L position
+    p.off.ps_posl = take(ps_on ? 4 * p.n : 0);                               // L position -> row
     p.off.ps_bperm = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);        // b in L-position order
     p.off.ps_yu = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);           // y in U'-position order
     p.off.total = o;

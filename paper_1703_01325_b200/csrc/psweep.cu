@@ -33,10 +33,11 @@ using namespace dev;
 namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
-constexpr int PS_NT = 2 * PS_NG;      // compute threads: two ping-pong groups
+constexpr int PS_NGRP = 2;            // compute groups (round-robin over records)
+constexpr int PS_NT = PS_NGRP * PS_NG; // compute threads
 constexpr int PS_NW = PS_NT / 32;     // compute warps; then producer, gather, poll warps
 constexpr int PS_NPOLL = 2;           // poll warps (alternate records)
-constexpr int PS_NAUX = 1 + PS_NPOLL; // producer + poll warps
+constexpr int PS_NAUX = 2 + PS_NPOLL; // two producers (even / odd records) + poll warps
 constexpr int PS_PF = 16;             // records prefetched into L2 ahead of their bulk copy
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -169,34 +170,42 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
     for (int x = tid; x < VS; x += blockDim.x) vring[size_t(x) * RS + a.ring_mask + 1] = 0.0;
     __syncthreads();
 
-    if (warp == PS_NW) {
-        // ============ producer: bulk copies into the record ring ===============
-        // per record two bulk copies on one mbarrier: the record's bytes and
-        // its rows' inputs (positions pos0 .. pos0+nr of b_perm for L, of y_u
-        // for U' -- the latter only once this part's L sweep is complete).
-        // Space is recycled in record order (empty barriers); records are
-        // pulled into L2 PS_PF ahead so the copies are short.
+    if (warp == PS_NW || warp == PS_NW + 1) {
+        // ============ producers: bulk copies into the record ring ==============
+        // producer pp serves records pp, pp+2, ... (the records of compute
+        // group pp) in its own half of the ring.  Per record two bulk copies on
+        // one mbarrier: the record's bytes and its rows' inputs (positions
+        // pos0 .. pos0+nr of b_perm for L, of y_u for U' -- the latter only once
+        // this part's L sweep is complete).  Space is recycled in record order
+        // (empty barriers); records are pulled into L2 ahead so the copies are short.
+        const int pp = warp - PS_NW;
+        const int nk = (nrec - pp + 1) / 2;   // records of this producer: pp + 2k
+        const uint32_t half = (a.data_bytes / 2) & ~15u;
+        unsigned char *ring = dring + pp * half;
         const uint64_t pol = policy_evict_first();
         uint32_t dhead = 0;
-        int oldest = 0;   // first record not yet known consumed
+        int oldest = 0;   // (own sequence) first record not yet known consumed
         int issued = 0;
         bool up_ready = false;
-        // record descriptors in registers, two windows of 32 (lane l: record base + l)
+        // record descriptors in registers, two windows of 32 (lane l: own record base + l)
         uint64_t cur_off = 0, nxt_off = 0;
         uint32_t cur_bytes = 0, cur_foot = 0, cur_pm = 0, nxt_bytes = 0, nxt_foot = 0, nxt_pm = 0;
         uint32_t cur_nr = 0, nxt_nr = 0;
-        auto fetch = [&](int j, uint64_t &off, uint32_t &bytes, uint32_t &foot, uint32_t &pos0u, uint32_t &nr) {
-            const PRecInfo &ri = a.rec[r0 + j];
+        auto fetch = [&](int k, uint64_t &off, uint32_t &bytes, uint32_t &foot, uint32_t &pos0u, uint32_t &nr) {
+            const PRecInfo &ri = a.rec[r0 + pp + 2 * k];
             off = ri.off;
             bytes = ri.bytes;
             foot = ri.foot;
             pos0u = uint32_t(ri.pos0) | (uint32_t(ri.level & 1) << 31);
             nr = uint32_t(ri.nrows);
         };
-        if (lane < nrec) fetch(lane, cur_off, cur_bytes, cur_foot, cur_pm, cur_nr);
-        if (32 + lane < nrec) fetch(32 + lane, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
-        for (int j = lane; j < PS_PF && j < nrec; j += 32) bulk_prefetch_l2(a.recs + cur_off, cur_bytes);
-        for (; issued < nrec; ++issued) {
+        auto wait_rec = [&](int rr) -> bool {   // record rr (any parity) consumed
+            return mbar_wait_or_abort(empty_bar + rr % K, uint32_t(rr / K) & 1u, &abort_flag, a);
+        };
+        if (lane < nk) fetch(lane, cur_off, cur_bytes, cur_foot, cur_pm, cur_nr);
+        if (32 + lane < nk) fetch(32 + lane, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
+        for (int j = lane; j < PS_PF / 2 && j < nk; j += 32) bulk_prefetch_l2(a.recs + cur_off, cur_bytes);
+        for (; issued < nk; ++issued) {
             if (issued > 0 && (issued & 31) == 0) {   // slide the window by 32 records
                 cur_off = nxt_off;
                 cur_bytes = nxt_bytes;
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                 cur_pm = nxt_pm;
                 cur_nr = nxt_nr;
                 const int j = issued + 32 + lane;
-                if (j < nrec) fetch(j, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
+                if (j < nk) fetch(j, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
             }
             const int jl = issued & 31;
             const uint64_t off = __shfl_sync(0xffffffffu, cur_off, jl);
@@ -214,53 +223,54 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             const uint32_t nr = __shfl_sync(0xffffffffu, cur_nr, jl);
             const bool up = pm >> 31;
             const uint32_t pos0 = pm & 0x7fffffffu;
+            const int rr = pp + 2 * issued;   // record index
             bool ok = true;
             if (up && !up_ready) {
-                // y_u is written by this part's L sweep: wait for every L record
-                // (both compute groups) before the first U' input copy
-                for (; ok && oldest < issued; ++oldest)
-                    ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                // y_u is written by this part's L sweep: every L record of both
+                // groups must be consumed before the first U' input copy
+                for (; ok && oldest < issued; ++oldest) ok = wait_rec(pp + 2 * oldest);
+                if (ok && rr >= 1) ok = wait_rec(rr - 1);
                 up_ready = true;
             }
-            // wait for a free ring slot and room for the footprint
+            // wait for a free ring slot and room for the footprint in this half
             int64_t at = -1;
             while (ok) {
-                if (issued - oldest >= K) {
-                    ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                if (issued - oldest >= K / 2) {
+                    ok = wait_rec(pp + 2 * oldest);
                     ++oldest;
                     continue;
                 }
                 const int live = issued - oldest;
-                at = ring_alloc(dhead, live ? slot_off[oldest % K] : 0, live, foot, a.data_bytes);
+                at = ring_alloc(dhead, live ? slot_off[(pp + 2 * oldest) % K] - pp * half : 0, live, foot, half);
                 if (at >= 0) break;
-                ok = mbar_wait_or_abort(empty_bar + oldest % K, uint32_t(oldest / K) & 1u, &abort_flag, a);
+                ok = wait_rec(pp + 2 * oldest);
                 ++oldest;
             }
             if (!ok) break;
-            const int si = issued % K;
-            // pull a record PS_PF ahead into L2 (no shared memory)
-            const int pf = issued + PS_PF;
+            const int si = rr % K;
+            // pull a record ahead into L2 (no shared memory)
+            const int pf = issued + PS_PF / 2;
             const int pj = pf - (issued & ~31);   // index into the two windows
             const uint64_t pf_off = __shfl_sync(0xffffffffu, pj < 32 ? cur_off : nxt_off, pj & 31);
             const uint32_t pf_bytes = __shfl_sync(0xffffffffu, pj < 32 ? cur_bytes : nxt_bytes, pj & 31);
             if (lane == 0) {
-                slot_off[si] = uint32_t(at);
+                slot_off[si] = uint32_t(at) + pp * half;
                 const uint32_t in_bytes = nr * uint32_t(VS * 8);
                 mbar_expect_tx(full_bar + si, bytes + in_bytes);
-                bulk_g2s(dring + at, a.recs + off, bytes, full_bar + si, pol);
-                bulk_g2s(dring + at + bytes, (up ? a.y_u : a.b_perm) + size_t(pos0) * VS, in_bytes, full_bar + si, pol);
-                if (pf < nrec && pj < 64) bulk_prefetch_l2(a.recs + pf_off, pf_bytes);
-                if (a.trace) a.trace[size_t(r0 + issued) * 8 + 0] = globaltimer();
+                bulk_g2s(ring + at, a.recs + off, bytes, full_bar + si, pol);
+                bulk_g2s(ring + at + bytes, (up ? a.y_u : a.b_perm) + size_t(pos0) * VS, in_bytes, full_bar + si, pol);
+                if (pf < nk && pj < 64) bulk_prefetch_l2(a.recs + pf_off, pf_bytes);
+                if (a.trace) a.trace[size_t(r0 + rr) * 8 + 0] = globaltimer();
             }
             __syncwarp();
         }
         // never leave the CTA with copies in flight into its shared memory
-        for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + g % K, uint32_t(g / K) & 1u);
-    } else if (warp > PS_NW) {
+        for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + (pp + 2 * g) % K, uint32_t((pp + 2 * g) / K) & 1u);
+    } else if (warp > PS_NW + 1) {
         // ============ poll: dependencies outside the on-chip ring ==============
         // warp p owns records p, p + NPOLL, ...; all its loads of a round are
         // in flight before any tag is checked (one L2 round trip per round)
-        const int pw = warp - PS_NW - 1;
+        const int pw = warp - PS_NW - 2;
         for (int i = pw; i < nrec; i += PS_NPOLL) {
             const int s = i % K;
             if (!mbar_wait_or_abort(full_bar + s, uint32_t(i / K) & 1u, &abort_flag, a)) break;
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
         const uint32_t vring_s = 0;   // the vector ring starts the dynamic shared memory
         auto lds = [&](uint32_t off) -> double { return *reinterpret_cast<const double *>(smem + off); };
         auto sts = [&](uint32_t off, double v) { *reinterpret_cast<double *>(smem + off) = v; };
-        for (int i = grp; i < nrec; i += 2) {
+        for (int i = grp; i < nrec; i += PS_NGRP) {
             const int s = i % K;
             const uint32_t ph = uint32_t(i / K) & 1u;
             if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) break;
@@ -336,21 +346,20 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
             const int nr = h.nrows, S = h.S, ng = h.nglob;
             const bool up = h.flags & 1;
-            const bool live = gt < nr;
+            const int n1 = (h.flags >> 1) & 0x1ff;   // rows of the record's first level; the rest are the next level
+            const int q2 = n1 + gt;                   // this thread's row of the second level
+            const bool live = gt < n1, live2 = q2 < nr;
             const int32_t *iarr = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr));
             const int32_t *desc = iarr + nr;
-            const double *vals = reinterpret_cast<const double *>(rec + h.vals_off) + gt + (up ? size_t(BS2) * nr : 0);
-            const double *inp = reinterpret_cast<const double *>(rec + h.in_off) + size_t(gt) * VS;
+            const double *vbase = reinterpret_cast<const double *>(rec + h.vals_off) + (up ? size_t(BS2) * nr : 0);
+            const double *vals = vbase + gt;
+            const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off);
             const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
-            double acc[BS];
-            double v[SR][BS2];
-            uint32_t xa[SR];   // shared address of component 0 of each staged dependency
-            uint32_t xs[SR];   // its component stride in bytes
-            int idx = 0;       // L: the row's U' position; U': its natural row
-            if (live) {
-                idx = iarr[gt];
-                if (up) {   // acc = D^-1 y: y is this part's own L result (no chain)
-                    const double *dv = vals - size_t(BS2) * nr;
+            // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
+            auto init_acc = [&](int q, double (&acc)[BS]) {
+                const double *inp = inp0 + size_t(q) * VS;
+                if (up) {
+                    const double *dv = vbase - size_t(BS2) * nr + q;
 #pragma unroll
                     for (int r = 0; r < BS; ++r) {
                         double z = dv[size_t(r) * nr] * inp[0];
@@ -362,6 +371,68 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
 #pragma unroll
                     for (int r = 0; r < BS; ++r) acc[r] = inp[r];
                 }
+            };
+            // slots [from, S) of row q straight from shared memory, 4 at a time
+            auto smem_slots = [&](int q, int from, double (&acc)[BS]) {
+                for (int sl0 = from; sl0 < S; sl0 += 4) {
+                    uint32_t ad[4], st[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t dd = sl0 + u < S ? desc[(sl0 + u) * nr + q] : a.ring_mask + 1;
+                        ad[u] = dd >= 0 ? vring_s + uint32_t(dd) * 8u : dep_s + uint32_t(-dd - 1) * 8u;
+                        st[u] = dd >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
+                    }
+                    double xv[4][BS];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) xv[u][c] = lds(ad[u] + uint32_t(c) * st[u]);
+                    double p2[4][BS];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double *vv = vbase + q + size_t(sl0 + u) * BS2 * nr;
+                        const bool on = sl0 + u < S;
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) p2[u][r] = on ? vv[size_t(r) * nr] * xv[u][0] : 0.0;
+#pragma unroll
+                        for (int c = 1; c < BS; ++c)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r)
+                                if (on) p2[u][r] = fma(vv[size_t(c * BS + r) * nr], xv[u][c], p2[u][r]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] -= (p2[0][r] + p2[1][r]) + (p2[2][r] + p2[3][r]);
+                }
+            };
+            // publish row q: ring (this part), tagged global vector (other parts),
+            // and y for this part's U' sweep (L) / the caller's x (U')
+            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
+                const uint32_t rs = vring_s + uint32_t((h.seq0 + q) & a.ring_mask) * 8u;
+#pragma unroll
+                for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
+                double pub[BS];
+#pragma unroll
+                for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
+                st_row<BS>((up ? a.x_t : a.y_t) + size_t(h.pos0 + q) * VS, pub);
+                if (up) {
+                    if (a.out) {
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) a.out[size_t(idx) * BS + r] = acc[r];
+                    }
+                } else {
+                    double *yu = a.y_u + size_t(idx) * VS;
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) yu[r] = acc[r];
+                }
+            };
+            double acc[BS], acc2[BS];
+            double v[SR][BS2];
+            uint32_t xa[SR];   // shared address of component 0 of each staged dependency
+            uint32_t xs[SR];   // its component stride in bytes
+            int idx = 0, idx2 = 0;   // L: the row's U' position; U': its natural row
+            if (live) {
+                idx = iarr[gt];
+                init_acc(gt, acc);
 #pragma unroll
                 for (int u = 0; u < SR; ++u) {
                     const int32_t d = u < S ? desc[u * nr + gt] : a.ring_mask + 1;
@@ -371,10 +442,14 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                     for (int e = 0; e < BS2; ++e) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
                 }
             }
+            if (live2) {
+                idx2 = iarr[q2];
+                init_acc(q2, acc2);
+            }
             if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
             if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 4] = globaltimer();
             // the other group has published record i-1
-            if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);
+            if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
             if (live) {
                 // register-staged slots: every dependency load first, then the
                 // products, summed as a tree and subtracted once
@@ -401,60 +476,21 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                         for (int r = 0; r < BS; ++r) pr[u][r] += pr[u + w][r];
 #pragma unroll
                 for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
-                // remaining slots straight from shared memory, 4 at a time:
-                // descriptors, dependencies and blocks loaded before the FMAs
-                for (int sl0 = SR; sl0 < S; sl0 += 4) {
-                    uint32_t ad[4], st[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int32_t dd = sl0 + u < S ? desc[(sl0 + u) * nr + gt] : a.ring_mask + 1;
-                        ad[u] = dd >= 0 ? vring_s + uint32_t(dd) * 8u : dep_s + uint32_t(-dd - 1) * 8u;
-                        st[u] = dd >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
-                    }
-                    double xv[4][BS];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int c = 0; c < BS; ++c) xv[u][c] = lds(ad[u] + uint32_t(c) * st[u]);
-                    double p2[4][BS];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const double *vv = vals + size_t(sl0 + u) * BS2 * nr;
-                        const bool on = sl0 + u < S;
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) p2[u][r] = on ? vv[size_t(r) * nr] * xv[u][0] : 0.0;
-#pragma unroll
-                        for (int c = 1; c < BS; ++c)
-#pragma unroll
-                            for (int r = 0; r < BS; ++r)
-                                if (on) p2[u][r] = fma(vv[size_t(c * BS + r) * nr], xv[u][c], p2[u][r]);
-                    }
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) acc[r] -= (p2[0][r] + p2[1][r]) + (p2[2][r] + p2[3][r]);
-                }
-                // publish: ring (this part), tagged global vector (other parts),
-                // and y for this part's U' sweep (L) / the caller's x (U')
-                const uint32_t rs = vring_s + uint32_t((h.seq0 + gt) & a.ring_mask) * 8u;
-#pragma unroll
-                for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
-                double pub[BS];
-#pragma unroll
-                for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
-                st_row<BS>((up ? a.x_t : a.y_t) + size_t(h.pos0 + gt) * VS, pub);
-                if (up) {
-                    if (a.out) {
-#pragma unroll
-                        for (int r = 0; r < BS; ++r) a.out[size_t(idx) * BS + r] = acc[r];
-                    }
-                } else {
-                    double *yu = a.y_u + size_t(idx) * VS;
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) yu[r] = acc[r];
+                smem_slots(gt, SR, acc);
+                publish(gt, idx, acc);
+            }
+            if (nr > n1) {
+                // the record's second level: its dependencies on the first level
+                // are in the ring once the group has passed this barrier
+                named_bar_sync(3 + grp, PS_NG);
+                if (live2) {
+                    smem_slots(q2, 0, acc2);
+                    publish(q2, idx2, acc2);
                 }
             }
             // hand record i+1 to the other group, release record i's ring space
             // (an L record's y_u stores are read later by the async proxy)
-            if (i + 1 < nrec) named_bar_arrive(1 + (grp ^ 1), 2 * PS_NG);
+            if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % PS_NGRP, 2 * PS_NG);
             if (!up) fence_proxy_async_global();
             mbar_arrive(empty_bar + s);
             if (a.trace && gt == 0) {
@@ -483,14 +519,17 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
 
 // b in L-position order (the L records' input bulk copies read it)
 template <int BS>
-__global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ posl, const double *__restrict__ b,
+__global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ lrow, const double *__restrict__ b,
                                  double *__restrict__ bp) {
+    // a gather: position p takes b's row lrow[p]; the writes (the costlier
+    // side of a permutation) are coalesced
     constexpr int VS = ps_vec_stride(BS);
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = __ldg(lrow + p);
         double v[VS];
 #pragma unroll
         for (int c = 0; c < VS; ++c) v[c] = c < BS ? __ldg(b + i * BS + c) : 0.0;
-        double *d = bp + size_t(__ldg(posl + i)) * VS;
+        double *d = bp + size_t(p) * VS;
         if constexpr (VS == 4) {
             reinterpret_cast<double4 *>(d)[0] = make_double4(v[0], v[1], v[2], v[3]);
         } else if constexpr (VS == 2) {

@@ -312,6 +312,18 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     const int32_t mask = ps.ring - 1;
     std::vector<int32_t> gl;     // a record's deduplicated dependency positions
     std::vector<int32_t> nfar;   // per row of a level group: dependencies outside the ring
+    // records pair two consecutive whole levels when both fit (a level step
+    // inside a record is a group barrier, not a pipeline stage); BILUK_PAIR=1 enables
+    bool pair_levels = false;   // measured neutral at 128^3 (few level pairs fit the record cap)
+    if (const char *env = std::getenv("BILUK_PAIR")) pair_levels = std::atoi(env) != 0;
+    struct Chunk {
+        size_t a, e;           // rows ord[a, e) of one level
+        int64_t lend;          // ring sequence number just past the level
+        bool whole;            // the chunk is its whole level
+        int S;
+        int64_t far;           // dependencies outside the ring (upper bound, not deduplicated)
+    };
+    std::vector<Chunk> chunks;
     for (int c = 0; c < P; ++c) {
         ps.part_rec[c] = int32_t(ps.rec.size());
         const int32_t b0 = pt.base[c];
@@ -323,25 +335,27 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
             const std::vector<int32_t> &pos = up ? ps.posU : ps.posL;
             const int32_t seq_base = up ? m : 0;   // ring sequence continues from the L sweep
             const size_t rec_begin = ps.rec.size();
+            // a dependency j of a row of a level ending at sequence `lend` is on
+            // chip iff it is in this part and the level's own writes cannot have
+            // recycled its ring slot
+            auto in_ring = [&](int32_t j, int64_t lend) {
+                return pt.part_of[j] == c && seq_base + int64_t(pos[j] - b0) >= lend - ps.ring;
+            };
+            // ---- chunks: <= nthreads rows of one level under the caps
+            chunks.clear();
             size_t g0 = 0;
             while (g0 < ord.size()) {
                 size_t ge = g0;
                 while (ge < ord.size() && lev[ord[ge]] == lev[ord[g0]]) ++ge;
-                const int64_t lvl_end_seq = seq_base + int64_t(ge);
-                // a dependency j of a row of this level is on chip iff it is in this part
-                // and the level's own writes cannot have recycled its ring slot
-                auto in_ring = [&](int32_t j) {
-                    return pt.part_of[j] == c && seq_base + int64_t(pos[j] - b0) >= lvl_end_seq - ps.ring;
-                };
+                const int64_t lend = seq_base + int64_t(ge);
                 nfar.assign(ge - g0, 0);
                 for (size_t q = g0; q < ge; ++q) {
                     const int32_t i = ord[q];
                     const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                    for (int32_t s = fs; s < fs + ns; ++s) nfar[q - g0] += in_ring(p.p_ci[s]) ? 0 : 1;
+                    for (int32_t s2 = fs; s2 < fs + ns; ++s2) nfar[q - g0] += in_ring(p.p_ci[s2], lend) ? 0 : 1;
                 }
                 size_t a = g0;
                 while (a < ge) {
-                    // greedy record: rows, footprint and fetched dependencies under their caps
                     size_t e = a;
                     int S = 0;
                     int64_t far = 0;
@@ -356,78 +370,98 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
                         far = far2;
                         ++e;
                     }
-                    const int nr = int(e - a);
-                    gl.clear();
-                    for (size_t q = a; q < e; ++q) {
-                        const int32_t i = ord[q];
-                        const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                        for (int32_t s = fs; s < fs + ns; ++s)
-                            if (!in_ring(p.p_ci[s])) gl.push_back(pos[p.p_ci[s]]);
-                    }
-                    std::sort(gl.begin(), gl.end());
-                    gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
-                    const int nglob = int(gl.size());
-                    const int64_t foot = rec_foot_bytes(bs2, vs, nr, S, nglob, up);
-                    if (nglob > ps.glob_cap || foot > ps.data_ring / 2 || foot >= (int64_t(1) << 31))
-                        return fail(BILUK_EUNSUPPORTED, "a block row is too long for the partitioned sweep");
-                    PRecInfo info{};
-                    info.nrows = nr;
-                    info.S = S;
-                    info.level = lev[ord[a]] * 2 + (up ? 1 : 0);
-                    info.nglob = nglob;
-                    info.pos0 = int32_t(b0 + int32_t(a));
-                    info.bytes = uint32_t(rec_total_bytes(bs2, nr, S, nglob, up));
-                    info.foot = uint32_t(foot);
-                    info.idx_words = uint32_t(rec_index_words(nr, S, nglob, up));
-                    info.off = uint64_t(ps.rec_total);
-                    info.idx_off = uint64_t(ps.idx.size());
-                    info.vmap_off = int64_t(ps.vmap.size());
-                    ps.rec_total += info.bytes;
-                    ps.max_rec = std::max<int64_t>(ps.max_rec, foot);
-                    ps.max_glob = std::max<int64_t>(ps.max_glob, nglob);
-                    ps.nglob_total += nglob;
-                    PRecHdr h{};
-                    h.nrows = nr;
-                    h.S = S;
-                    h.nglob = nglob;
-                    h.flags = lev[ord[a]] * 2 + (up ? 1 : 0);
-                    h.seq0 = int32_t(seq_base + int32_t(a));
-                    h.pos0 = int32_t(b0 + int32_t(a));
-                    h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
-                    h.in_off = int32_t(info.bytes);
-                    const size_t base = ps.idx.size();
-                    ps.idx.resize(base + size_t(a16(4 * int64_t(info.idx_words)) / 4), 0);   // 16-byte aligned sections
-                    std::memcpy(ps.idx.data() + base, &h, sizeof(h));
-                    int32_t *w = ps.idx.data() + base + sizeof(PRecHdr) / 4;
-                    for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
-                    w += nr;
-                    int32_t *desc = w;
-                    int32_t *gpos = w + int64_t(S) * nr;
-                    for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
-                    const size_t vbase = ps.vmap.size();
-                    ps.vmap.resize(vbase + size_t(S) * nr, -1);
-                    for (int q = 0; q < nr; ++q) {
-                        const int32_t i = ord[a + q];
-                        const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                        for (int s = 0; s < S; ++s) {
-                            int32_t d = ps.ring;   // zero slot
-                            if (s < ns) {
-                                const int32_t j = p.p_ci[fs + s];
-                                if (in_ring(j)) {
-                                    d = int32_t((seq_base + int64_t(pos[j] - b0)) & mask);
-                                } else {
-                                    const int64_t at = std::lower_bound(gl.begin(), gl.end(), pos[j]) - gl.begin();
-                                    d = -int32_t(at) - 1;   // fetched dependency `at`
-                                }
-                                ps.vmap[vbase + size_t(s) * nr + q] = fs + s;
-                            }
-                            desc[int64_t(s) * nr + q] = d;
-                        }
-                    }
-                    ps.rec.push_back(info);
+                    chunks.push_back({a, e, lend, a == g0 && e == ge, S, far});
                     a = e;
                 }
                 g0 = ge;
+            }
+            // ---- records: one chunk, or two whole consecutive levels
+            for (size_t ci0 = 0; ci0 < chunks.size();) {
+                size_t ncs = 1;
+                if (pair_levels && ci0 + 1 < chunks.size()) {
+                    const Chunk &c1 = chunks[ci0], &c2 = chunks[ci0 + 1];
+                    const int nr = int(c2.e - c1.a);
+                    const int S2 = std::max(c1.S, c2.S);
+                    if (c1.whole && c2.whole && c1.e - c1.a <= 255 && c2.e - c2.a <= size_t(ps.nthreads) &&
+                        c1.far + c2.far <= ps.glob_cap && rec_foot_bytes(bs2, vs, nr, S2, int(c1.far + c2.far), up) <= ps.rec_cap)
+                        ncs = 2;
+                }
+                const size_t a = chunks[ci0].a, e = chunks[ci0 + ncs - 1].e;
+                const int nr = int(e - a);
+                const int n1 = int(chunks[ci0].e - a);
+                int S = 0;
+                for (size_t k2 = 0; k2 < ncs; ++k2) S = std::max(S, chunks[ci0 + k2].S);
+                auto lend_of = [&](size_t q) { return q < chunks[ci0].e ? chunks[ci0].lend : chunks[ci0 + ncs - 1].lend; };
+                gl.clear();
+                for (size_t q = a; q < e; ++q) {
+                    const int32_t i = ord[q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int32_t s2 = fs; s2 < fs + ns; ++s2)
+                        if (!in_ring(p.p_ci[s2], lend_of(q))) gl.push_back(pos[p.p_ci[s2]]);
+                }
+                std::sort(gl.begin(), gl.end());
+                gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+                const int nglob = int(gl.size());
+                const int64_t foot = rec_foot_bytes(bs2, vs, nr, S, nglob, up);
+                if (nglob > ps.glob_cap || foot > ps.data_ring / 4 || foot >= (int64_t(1) << 31))   // half a producer's half ring
+                    return fail(BILUK_EUNSUPPORTED, "a block row is too long for the partitioned sweep");
+                const int32_t lvl = lev[ord[a]];
+                PRecInfo info{};
+                info.nrows = nr;
+                info.S = S;
+                info.level = lvl * 2 + (up ? 1 : 0);
+                info.nglob = nglob;
+                info.pos0 = int32_t(b0 + int32_t(a));
+                info.bytes = uint32_t(rec_total_bytes(bs2, nr, S, nglob, up));
+                info.foot = uint32_t(foot);
+                info.idx_words = uint32_t(rec_index_words(nr, S, nglob, up));
+                info.off = uint64_t(ps.rec_total);
+                info.idx_off = uint64_t(ps.idx.size());
+                info.vmap_off = int64_t(ps.vmap.size());
+                ps.rec_total += info.bytes;
+                ps.max_rec = std::max<int64_t>(ps.max_rec, foot);
+                ps.max_glob = std::max<int64_t>(ps.max_glob, nglob);
+                ps.nglob_total += nglob;
+                PRecHdr h{};
+                h.nrows = nr;
+                h.S = S;
+                h.nglob = nglob;
+                h.flags = (up ? 1 : 0) | (n1 << 1) | (lvl << 10);
+                h.seq0 = int32_t(seq_base + int32_t(a));
+                h.pos0 = int32_t(b0 + int32_t(a));
+                h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
+                h.in_off = int32_t(info.bytes);
+                const size_t base = ps.idx.size();
+                ps.idx.resize(base + size_t(a16(4 * int64_t(info.idx_words)) / 4), 0);   // 16-byte aligned sections
+                std::memcpy(ps.idx.data() + base, &h, sizeof(h));
+                int32_t *w = ps.idx.data() + base + sizeof(PRecHdr) / 4;
+                for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
+                w += nr;
+                int32_t *desc = w;
+                int32_t *gpos = w + int64_t(S) * nr;
+                for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
+                const size_t vbase = ps.vmap.size();
+                ps.vmap.resize(vbase + size_t(S) * nr, -1);
+                for (int q = 0; q < nr; ++q) {
+                    const int32_t i = ord[a + q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        int32_t d = ps.ring;   // zero slot
+                        if (s2 < ns) {
+                            const int32_t j = p.p_ci[fs + s2];
+                            if (in_ring(j, lend_of(a + q))) {
+                                d = int32_t((seq_base + int64_t(pos[j] - b0)) & mask);
+                            } else {
+                                const int64_t at = std::lower_bound(gl.begin(), gl.end(), pos[j]) - gl.begin();
+                                d = -int32_t(at) - 1;   // fetched dependency `at`
+                            }
+                            ps.vmap[vbase + size_t(s2) * nr + q] = fs + s2;
+                        }
+                        desc[int64_t(s2) * nr + q] = d;
+                    }
+                }
+                ps.rec.push_back(info);
+                ci0 += ncs;
             }
             if (!up) ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
         }
