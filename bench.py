@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip ILU(2), BiCGSTAB and CPU baseline legs")
     ap.add_argument("--cpu-nx", type=int, default=64, help="grid edge of the CPU-baseline sample")
+    ap.add_argument("--batch", type=int, default=64, help="systems of the batch leg (configs[4]); 0 skips it")
     return ap.parse_args()
 
 
@@ -271,6 +272,49 @@ def main():
                                     "frac_of_measured_hbm": B2 / (ms2 * 1e-3) / 1e9 / peak, "setup_s": s2,
                                     "levels": [f2.info["levels_L"], f2.info["levels_U"]]}
             del f2
+
+    if not args.no_extras and args.batch > 0:
+        # BASELINE configs[4]: a batch of independent 64^3 b3 systems, ILU(1),
+        # 64 / N per rank, applied as ONE block-diagonal operator (their level
+        # chains interleave in one persistent sweep); weak over ranks
+        nsys = max(1, args.batch // world)
+        t0 = time.perf_counter()
+        mats = []
+        for sidx in range(nsys):
+            nb_, bs_, rp_, ci_, v_ = b2.reservoir_block_grid(64, 64, 64, args.bs, seed=rank * nsys + sidx)
+            mats.append(b2.BcsrMatrix(bs_, nb_, nb_, rp_, ci_, v_))
+        big = b2.block_diagonal(mats)
+        del mats
+        t1 = time.perf_counter()
+        fb = b2.build_preconditioner(big, 1)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        Bb = apply_bytes(fb.info)
+        rb = torch.from_numpy(np.random.default_rng(1).standard_normal(big.shape[0])).cuda()
+        ob = torch.empty_like(rb)
+        for _ in range(3):
+            b2.apply_preconditioner(fb, rb, out=ob)
+        barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(5):
+            b2.apply_preconditioner(fb, rb, out=ob)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        fb.status()
+        msb = q0.elapsed_time(q1) / 5
+        if dist is not None:
+            tt = torch.tensor([msb], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            msb = float(tt.item())
+        extras["batch_apply"] = {
+            "workload": f"{nsys * world} x 64^3 b{args.bs} ILU(1), {nsys} per GPU as one block-diagonal operator",
+            "ms": msb, "GBps_aggregate": world * Bb / (msb * 1e-3) / 1e9,
+            "frac_of_measured_hbm_per_gpu": Bb / (msb * 1e-3) / 1e9 / peak,
+            "system_applies_per_s": world * nsys / (msb * 1e-3), "setup_s": t2 - t1, "gen_s": t1 - t0,
+            "engine": fb.info["engine"]}
+        del fb, big, rb, ob
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and not args.no_extras:

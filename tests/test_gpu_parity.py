@@ -213,3 +213,21 @@ def test_both_engines_match_oracle_and_are_repeatable(b2, monkeypatch, engine, c
     for _ in range(3):
         assert torch.equal(b2.apply_preconditioner(f, rt), x1)
     f.status()
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_block_diagonal_batch_equals_independent_systems(b2, k):
+    """A batch applied as one block-diagonal operator equals each system alone."""
+    mats, rhs = [], []
+    for s in range(3):
+        n, bs, rp, ci, vals = b2.reservoir_block_grid(7 + s, 6, 5, 3, seed=20 + s)
+        mats.append((n, bs, rp, ci, vals))
+        rhs.append(np.random.default_rng(s).standard_normal(n * bs))
+    big = b2.block_diagonal([b2.BcsrMatrix(bs, n, n, rp, ci, vals) for n, bs, rp, ci, vals in mats])
+    f = b2.build_preconditioner(big, k)
+    z = b2.apply_preconditioner(f, np.concatenate(rhs))
+    off = 0
+    for (n, bs, rp, ci, vals), r in zip(mats, rhs):
+        want = orc.build_preconditioner(n, bs, rp, ci, vals, k).apply(r)
+        assert rel_err(z[off:off + n * bs], want) <= TOL
+        off += n * bs

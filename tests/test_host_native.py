@@ -207,3 +207,29 @@ def test_partitioned_sweep_plan_geometry():
             assert nrec == info["records"] > 0
         finally:
             L.biluk_plan_destroy(h)
+
+
+def test_block_diagonal_batch_assembly():
+    """Batch assembly: offsets, values and the decoupled ILU(k) pattern."""
+    ms = [b2.reservoir_block_grid(3 + s, 3, 2, 2, seed=s) for s in range(3)]
+    big = b2.block_diagonal([b2.BcsrMatrix(bs, n, n, rp, ci, v) for n, bs, rp, ci, v in ms])
+    assert big.shape == (sum(n for n, *_ in ms) * 2,) * 2
+    r = z = 0
+    for n, bs, rp, ci, v in ms:
+        assert np.array_equal(big.row_ptr[r:r + n + 1] - big.row_ptr[r], rp)
+        assert np.array_equal(big.col_idx[z:z + rp[-1]] - r, ci)
+        assert np.array_equal(big.values[z * 4:(z + rp[-1]) * 4], v)
+        r += n
+        z += rp[-1]
+    # the symbolic phase of the batch is the per-system patterns, shifted
+    pb = b2.symbolic_phase(b2.extract_point_pattern(big) if False else b2.PatternMatrix.from_csr_arrays(
+        big.num_block_rows, big.row_ptr, big.col_idx), 1)
+    rb, cb = pb.to_csr_arrays()
+    r = z = 0
+    for n, bs, rp, ci, v in ms:
+        p1 = b2.symbolic_phase(b2.PatternMatrix.from_csr_arrays(n, rp, ci), 1)
+        r1, c1 = p1.to_csr_arrays()
+        assert np.array_equal(rb[r:r + n + 1] - rb[r], r1) and np.array_equal(cb[rb[r]:rb[r + n]] - r, c1)
+        r += n
+    with pytest.raises(b2.StructuralError):
+        b2.block_diagonal([b2.BcsrMatrix(2, 1, 1, [0, 1], [0], np.ones(4)), b2.BcsrMatrix(3, 1, 1, [0, 1], [0], np.ones(9))])
