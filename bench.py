@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip ILU(2), BiCGSTAB and CPU baseline legs")
     ap.add_argument("--cpu-nx", type=int, default=64, help="grid edge of the CPU-baseline sample")
     ap.add_argument("--batch", type=int, default=64, help="systems of the batch leg (configs[4]); 0 skips it")
+    ap.add_argument("--configs", type=int, default=1, help="time-to-solution on configs[0,1,3] (0 skips)")
     return ap.parse_args()
 
 
@@ -272,6 +273,38 @@ def main():
                                     "frac_of_measured_hbm": B2 / (ms2 * 1e-3) / 1e9 / peak, "setup_s": s2,
                                     "levels": [f2.info["levels_L"], f2.info["levels_U"]]}
             del f2
+
+    if not args.no_extras and args.configs:
+        # time-to-solution on the other BASELINE configs (b = A 1, x0 = 0,
+        # relative tolerance 1e-6; setup = build_preconditioner, reported apart)
+        runs = {}
+        for name, (nxc, bsc, kc, solver) in {
+                "cfg0_16^3_b3_ILU0_bicgstab": (16, 3, 0, "bicgstab"),
+                "cfg1_64^3_b3_ILU1_bicgstab": (64, 3, 1, "bicgstab"),
+                "cfg3_100^3_b4_ILU1_gmres30": (100, 4, 1, "gmres"),
+                "cfg3_100^3_b8_ILU1_gmres30": (100, 8, 1, "gmres")}.items():
+            ncf, bsf, rpf, cif, vf = b2.reservoir_block_grid(nxc, nxc, nxc, bsc, seed=rank)
+            af = b2.BcsrMatrix(bsf, ncf, ncf, rpf, cif, vf)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ff = b2.build_preconditioner(af, kc)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            bb = torch.from_numpy(b2.synthetic.ones_rhs(ncf, bsf, rpf, cif, vf)).cuda()
+            cfgf = b2.SolverConfig(restart=30, rel_tol=1e-6)
+            solve = b2.bicgstab if solver == "bicgstab" else b2.gmres
+            solve(af, bb, M=ff, cfg=cfgf)   # warm (operator upload, workspace)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            _, stf = solve(af, bb, M=ff, cfg=cfgf)
+            torch.cuda.synchronize()
+            t3 = time.perf_counter()
+            runs[name] = {"solve_s": t3 - t2, "iterations": stf.iterations, "converged": stf.converged,
+                          "true_rel_residual": stf.final_relative_residual, "setup_s": t1 - t0,
+                          "engine": ff.info["engine"]}
+            del ff, af, bb
+            torch.cuda.empty_cache()
+        extras["configs"] = runs
 
     if not args.no_extras and args.batch > 0:
         # BASELINE configs[4]: a batch of independent 64^3 b3 systems, ILU(1),
