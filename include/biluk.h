@@ -191,6 +191,19 @@ int biluk_gmres(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user,
                 double *dev_x, void *dev_work, int32_t restart, int64_t max_iters, double rel_tol,
                 double abs_tol, double *stats, double *history, int64_t hist_cap, void *stream);
 
+/* Batched BiCGSTAB over nsys independent systems packed as ONE block-diagonal
+ * operator A (and one preconditioner M factored over it, e.g. from
+ * biluk_bind of the block-diagonal pattern): system s owns block rows
+ * [seg[s], seg[s+1]) (host array, seg[0] = 0, seg[nsys] = n; the caller
+ * guarantees A has no entries coupling two segments).  Each system runs the
+ * iteration of biluk_bicgstab with its own scalars and stopping tests (the
+ * single solve's result up to the preconditioner's rounding); SpMV and
+ * preconditioner sweeps run once per step over all systems.  stats: 4 doubles per system, as biluk_bicgstab. */
+uint64_t biluk_krylov_batched_workspace_bytes(int64_t len, int32_t nsys);
+int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user, int32_t nsys,
+                           const int64_t *seg, const double *dev_b, double *dev_x, void *dev_work,
+                           int64_t max_iters, double rel_tol, double *stats, void *stream);
+
 /* Deterministic FP64 dot product of two device vectors (fixed reduction tree). */
 int biluk_dot(const double *dev_a, const double *dev_b, int64_t len, double *result, void *dev_work,
               void *stream);

@@ -64,6 +64,9 @@ _SIGS = {
                                       P_dbl, P_dbl, c_i64, c_vp]),
     "biluk_gmres": (ctypes.c_int, [c_vp, c_vp, PRECOND_FN, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_dbl, c_dbl,
                                    P_dbl, P_dbl, c_i64, c_vp]),
+    "biluk_krylov_batched_workspace_bytes": (c_u64, [c_i64, c_i32]),
+    "biluk_bicgstab_batched": (ctypes.c_int, [c_vp, c_vp, PRECOND_FN, c_vp, c_i32, P_i64, c_vp, c_vp, c_vp, c_i64,
+                                              c_dbl, P_dbl, c_vp]),
     "biluk_dot": (ctypes.c_int, [c_vp, c_vp, c_i64, P_dbl, c_vp, c_vp]),
 }
 

@@ -28,7 +28,9 @@ constexpr int MAXQ = 3;
 // scalar slots in DevStatus::scal
 enum {
     S_RHO = 0, S_RHO_PREV, S_ALPHA, S_OMEGA, S_BETA, S_RV, S_SS, S_TT, S_TS, S_RR, S_RHO_NEXT, S_GEN0, S_GEN1,
-    S_GEN2, S_HPREV, S_H0 = 16   // S_H0.. : scratch for the current GMRES column
+    S_GEN2, S_HPREV, S_H0 = 16,  // S_H0.. : scratch for the current GMRES column
+    // batched BiCGSTAB (per-system block of B_STRIDE slots; S_H0.. unused there)
+    S_BN = 16, S_XA, S_XW, S_ITS, S_NH, S_LAST, S_TRUE, B_STRIDE = 24
 };
 
 __device__ __forceinline__ double block_sum(double v, double *sh) {
@@ -61,15 +63,34 @@ struct Fused {
     const double *qb[MAXQ];   // dot q: qa[q] . qb[q]; nullptr means "the updated u"
 };
 
+// Batched form (independent systems packed back to back, biluk_bicgstab_batched):
+// block sys * RED_BLOCKS + j reduces chunk j of system sys's segment
+// [seg[sys], seg[sys+1]) -- the same partition a single solve of that system
+// uses, so a system's reductions round as in its own solve.  `state`
+// gates the update per system (skipped when state[sys] > smax).
+struct Batch {
+    const int64_t *seg;   // nullptr: one system [0, len)
+    const int *state;
+    int smax;
+    int sstride;          // scalar slots per system
+};
+
 __global__ void __launch_bounds__(RED_THREADS) fused_kernel(Fused f, int64_t len, const double *scal, double *partials,
-                                                            const int *skip) {
+                                                            const int *skip, Batch bt) {
     __shared__ double sh[RED_THREADS];
     if (skip && *skip) return;
+    const int sys = blockIdx.x / RED_BLOCKS;
+    const int blk = blockIdx.x % RED_BLOCKS;
+    if (bt.state && bt.state[sys] > bt.smax) return;
+    const int64_t base = bt.seg ? bt.seg[sys] : 0;
+    const int64_t slen = bt.seg ? bt.seg[sys + 1] - base : len;
+    scal += int64_t(sys) * bt.sstride;
+    partials += int64_t(sys) * MAXQ * RED_BLOCKS;
     const double c0 = f.ic0 >= 0 ? f.sgn0 * scal[f.ic0] : 0.0;
     const double c1 = f.ic1 >= 0 ? scal[f.ic1] : 0.0;
-    const int64_t chunk = (len + RED_BLOCKS - 1) / RED_BLOCKS;
-    const int64_t lo = int64_t(blockIdx.x) * chunk;
-    const int64_t hi = lo + chunk < len ? lo + chunk : len;
+    const int64_t chunk = (slen + RED_BLOCKS - 1) / RED_BLOCKS;
+    const int64_t lo = base + int64_t(blk) * chunk;
+    const int64_t hi = lo + chunk < base + slen ? lo + chunk : base + slen;
     double acc[MAXQ] = {0.0, 0.0, 0.0};
     for (int64_t i = lo + threadIdx.x; i < hi; i += RED_THREADS) {
         double uval = 0.0;
@@ -89,17 +110,30 @@ __global__ void __launch_bounds__(RED_THREADS) fused_kernel(Fused f, int64_t len
     }
     for (int q = 0; q < f.nq; ++q) {
         const double s = block_sum(acc[q], sh);
-        if (threadIdx.x == 0) partials[q * RED_BLOCKS + blockIdx.x] = s;
+        if (threadIdx.x == 0) partials[q * RED_BLOCKS + blk] = s;
     }
 }
 
 // Second pass: sum the partials of nq dots in fixed order into scal[dst[q]],
-// then run the scalar epilogue `op`.
-enum { FIN_NONE = 0, FIN_ALPHA, FIN_OMEGA, FIN_BETA, FIN_DIV, FIN_GMRES_H };
+// then run the scalar epilogue `op`.  One block per system.
+enum { FIN_NONE = 0, FIN_ALPHA, FIN_OMEGA, FIN_BETA, FIN_DIV, FIN_GMRES_H,
+       FIN_B_INIT, FIN_B_ALPHA, FIN_B_HALF, FIN_B_OMEGA, FIN_B_BETA, FIN_B_TRUE };
+
+// batched per-system state: 0 iterating, 1 finishing (x update pending), 2 stopped
+struct BFin {
+    int *state;
+    double tol;
+    int64_t it;
+};
+
 __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double *partials, int nq, int d0, int d1, int d2,
-                                                               int op, double *scal, const int *skip) {
+                                                               int op, double *scal, const int *skip, int sstride,
+                                                               BFin bf) {
     __shared__ double sh[RED_THREADS];
     if (skip && *skip) return;
+    const int sys = blockIdx.x;
+    partials += int64_t(sys) * MAXQ * RED_BLOCKS;
+    scal += int64_t(sys) * sstride;
     const int dst[3] = {d0, d1, d2};
     for (int q = 0; q < nq; ++q) {
         double v = 0.0;
@@ -107,21 +141,69 @@ __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double *par
         const double s = block_sum(v, sh);
         if (threadIdx.x == 0) scal[dst[q]] = s;
     }
-    if (threadIdx.x == 0) {
-        switch (op) {
-            case FIN_ALPHA:   // alpha = rho / <r^, v>
-                if (scal[S_RV] != 0.0) scal[S_ALPHA] = scal[S_RHO] / scal[S_RV];
-                break;
-            case FIN_OMEGA:   // omega = <t, s> / <t, t>
-                if (scal[S_TT] != 0.0) scal[S_OMEGA] = scal[S_TS] / scal[S_TT];
-                break;
-            case FIN_BETA:    // next iteration: beta = (rho_n / rho)(alpha / omega); rho <- rho_n
-                scal[S_BETA] = (scal[S_RHO_NEXT] / scal[S_RHO]) * (scal[S_ALPHA] / scal[S_OMEGA]);
-                scal[S_RHO_PREV] = scal[S_RHO];
-                scal[S_RHO] = scal[S_RHO_NEXT];
-                break;
-            default: break;
+    if (threadIdx.x != 0) return;
+    int *st = bf.state ? bf.state + sys : nullptr;
+    switch (op) {
+        case FIN_ALPHA:   // alpha = rho / <r^, v>
+            if (scal[S_RV] != 0.0) scal[S_ALPHA] = scal[S_RHO] / scal[S_RV];
+            break;
+        case FIN_OMEGA:   // omega = <t, s> / <t, t>
+            if (scal[S_TT] != 0.0) scal[S_OMEGA] = scal[S_TS] / scal[S_TT];
+            break;
+        case FIN_BETA:    // next iteration: beta = (rho_n / rho)(alpha / omega); rho <- rho_n
+            scal[S_BETA] = (scal[S_RHO_NEXT] / scal[S_RHO]) * (scal[S_ALPHA] / scal[S_OMEGA]);
+            scal[S_RHO_PREV] = scal[S_RHO];
+            scal[S_RHO] = scal[S_RHO_NEXT];
+            break;
+        // ---- batched BiCGSTAB: the host-side tests of biluk_bicgstab, per system ----
+        case FIN_B_INIT: {   // S_GEN0 = <b, b>
+            const double bb = scal[S_GEN0];
+            scal[S_BN] = sqrt(bb);
+            scal[S_RHO] = bb; scal[S_RHO_PREV] = 1.0; scal[S_ALPHA] = 1.0; scal[S_OMEGA] = 1.0; scal[S_BETA] = bb;
+            scal[S_ITS] = 0.0; scal[S_NH] = 0.0; scal[S_LAST] = INFINITY;
+            *st = bb == 0.0 ? 2 : 0;
+            if (bb == 0.0) scal[S_LAST] = 0.0;
+            break;
         }
+        case FIN_B_ALPHA:
+            if (*st != 0) break;
+            if (scal[S_RV] == 0.0) { *st = 2; break; }   // breakdown before the iteration counts
+            scal[S_ALPHA] = scal[S_RHO] / scal[S_RV];
+            scal[S_ITS] = double(bf.it);
+            break;
+        case FIN_B_HALF: {
+            if (*st != 0) break;
+            const double sn = sqrt(scal[S_SS]) / scal[S_BN];
+            scal[S_LAST] = sn;
+            if (sn <= bf.tol) {   // x += alpha p^, stop
+                scal[S_XA] = scal[S_ALPHA]; scal[S_XW] = 0.0; scal[S_NH] += 1.0; *st = 1;
+            }
+            break;
+        }
+        case FIN_B_OMEGA:
+            if (*st != 0) break;
+            scal[S_XA] = scal[S_ALPHA];
+            if (scal[S_TT] == 0.0) { scal[S_XW] = 0.0; scal[S_NH] += 1.0; *st = 1; break; }
+            scal[S_OMEGA] = scal[S_TS] / scal[S_TT];
+            scal[S_XW] = scal[S_OMEGA];
+            break;
+        case FIN_B_BETA: {
+            if (*st == 1) { *st = 2; break; }
+            if (*st != 0) break;
+            const double rn = sqrt(scal[S_RR]) / scal[S_BN];
+            scal[S_LAST] = rn;
+            scal[S_NH] += 1.0;
+            const double om = scal[S_OMEGA];
+            scal[S_BETA] = (scal[S_RHO_NEXT] / scal[S_RHO]) * (scal[S_ALPHA] / om);
+            scal[S_RHO_PREV] = scal[S_RHO];
+            scal[S_RHO] = scal[S_RHO_NEXT];
+            if (rn <= bf.tol || om == 0.0 || scal[S_RHO] == 0.0) *st = 2;
+            break;
+        }
+        case FIN_B_TRUE:   // S_GEN1 = ||b - A x||^2
+            scal[S_TRUE] = scal[S_BN] == 0.0 ? 0.0 : sqrt(scal[S_GEN1]) / scal[S_BN];
+            break;
+        default: break;
     }
 }
 
@@ -159,15 +241,25 @@ struct Ctx {
     double *partials;
     int grid;
     cudaError_t err = cudaSuccess;
+    // batched solves (biluk_bicgstab_batched); defaults describe one system
+    int nsys = 1;
+    const int64_t *seg = nullptr;
+    int *state = nullptr;
+    int smax = 0;
+    int sstride = 0;
+    double tol = 0.0;
+    int64_t it = 0;
 
     void fused(const Fused &f) {
         if (err) return;
-        fused_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(f, len, scal, partials, nullptr);
+        fused_kernel<<<RED_BLOCKS * nsys, RED_THREADS, 0, s>>>(f, len, scal, partials, nullptr,
+                                                                Batch{seg, state, smax, sstride});
         err = cudaGetLastError();
     }
     void fin(int nq, int d0, int d1, int d2, int op) {
         if (err) return;
-        finalize_kernel<<<1, RED_THREADS, 0, s>>>(partials, nq, d0, d1, d2, op, scal, nullptr);
+        finalize_kernel<<<nsys, RED_THREADS, 0, s>>>(partials, nq, d0, d1, d2, op, scal, nullptr, sstride,
+                                                     BFin{state, tol, it});
         err = cudaGetLastError();
     }
     void dot(const double *a, const double *b, int dst) {
@@ -256,8 +348,9 @@ int biluk_dot(const double *dev_a, const double *dev_b, int64_t len, double *res
     f.nq = 1;
     f.qa[0] = dev_a;
     f.qb[0] = dev_b;
-    fused_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(f, len, scal, partials, nullptr);
-    finalize_kernel<<<1, RED_THREADS, 0, s>>>(partials, 1, 0, 0, 0, FIN_NONE, scal, nullptr);
+    fused_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(f, len, scal, partials, nullptr, Batch{nullptr, nullptr, 0, 0});
+    finalize_kernel<<<1, RED_THREADS, 0, s>>>(partials, 1, 0, 0, 0, FIN_NONE, scal, nullptr, 0,
+                                              BFin{nullptr, 0.0, 0});
     cudaError_t e = cudaMemcpyAsync(result, scal, 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(BILUK_ECUDA, std::string("dot: ") + cudaGetErrorString(e));
@@ -405,6 +498,151 @@ int biluk_bicgstab(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *us
     stats[1] = rel <= rel_tol ? 1 : 0;
     stats[2] = rel;
     stats[3] = double(nh);
+    return M ? biluk_plan_status(M, stream) : BILUK_OK;
+}
+
+uint64_t biluk_krylov_batched_workspace_bytes(int64_t len_, int32_t nsys) {
+    if (len_ < 0 || nsys < 1) return 0;
+    const uint64_t len = uint64_t(len_);
+    const uint64_t vec = ((8 * len + 255) / 256) * 256;
+    const uint64_t ns = uint64_t(nsys);
+    return 8 * vec + 8 * RED_BLOCKS * MAXQ * ns + 8 * B_STRIDE * ns + 8 * (ns + 1) + 4 * ns + 4096;
+}
+
+// Batched BiCGSTAB: nsys independent systems packed as one block-diagonal
+// operator (system s = block rows [seg[s], seg[s+1])) and one preconditioner
+// over it.  Every system runs exactly the iteration of biluk_bicgstab on its
+// own segment -- its own scalars, stopping tests and iteration count, with the
+// same reduction partition as a single solve (x_s equals the single solve's up
+// to the rounding of the preconditioner, whose record layout differs in a
+// batch) -- while the SpMV and the preconditioner sweeps cover all systems in
+// one launch each (their level chains interleave).  A stopped system is frozen;
+// the loop ends when every system has stopped.
+int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user, int32_t nsys,
+                           const int64_t *seg, const double *dev_b, double *dev_x, void *dev_work, int64_t max_iters,
+                           double rel_tol, double *stats, void *stream) {
+    if (!A || !A->o.valued) return fail(BILUK_EARG, "operator has no values");
+    if (A->o.n != A->o.ncols) return fail(BILUK_EARG, "bicgstab requires a square matrix");
+    if (M && (!M->p.factored || M->p.n != A->o.n || M->p.bs != A->o.bs))
+        return fail(BILUK_EARG, "preconditioner does not match the operator");
+    if (max_iters < 1 || !(rel_tol > 0.0)) return fail(BILUK_EARG, "bad solver configuration");
+    if (nsys < 1 || !seg || !stats) return fail(BILUK_EARG, "bad batch description");
+    if (seg[0] != 0 || seg[nsys] != A->o.n) return fail(BILUK_EARG, "batch segments must cover [0, n)");
+    for (int32_t i = 0; i < nsys; ++i)
+        if (seg[i + 1] < seg[i]) return fail(BILUK_EARG, "batch segments must be non-decreasing");
+    const int64_t bs = A->o.bs;
+    const int64_t len = A->o.n * bs;
+    const int32_t precond = (M || cb) ? 1 : 0;
+    const uint64_t vec = ((8 * uint64_t(len) + 255) / 256) * 256;
+    unsigned char *w = static_cast<unsigned char *>(dev_work);
+    double *r = reinterpret_cast<double *>(w + 0 * vec);
+    double *rh = reinterpret_cast<double *>(w + 1 * vec);
+    double *pv = reinterpret_cast<double *>(w + 2 * vec);
+    double *v = reinterpret_cast<double *>(w + 3 * vec);
+    double *ph = reinterpret_cast<double *>(w + 4 * vec);
+    double *sv = reinterpret_cast<double *>(w + 5 * vec);
+    double *sh = reinterpret_cast<double *>(w + 6 * vec);
+    double *t = reinterpret_cast<double *>(w + 7 * vec);
+    double *partials = reinterpret_cast<double *>(w + 8 * vec);
+    double *scal = partials + int64_t(RED_BLOCKS) * MAXQ * nsys;
+    int64_t *dseg = reinterpret_cast<int64_t *>(scal + int64_t(B_STRIDE) * nsys);
+    int *dstate = reinterpret_cast<int *>(dseg + nsys + 1);
+    Ctx c{A, M, cb, user, static_cast<cudaStream_t>(stream), len, scal, partials, 0};
+    c.nsys = nsys;
+    c.seg = dseg;
+    c.state = dstate;
+    c.sstride = B_STRIDE;
+    c.tol = rel_tol;
+    std::vector<int64_t> hseg(nsys + 1);
+    for (int32_t i = 0; i <= nsys; ++i) hseg[i] = seg[i] * bs;
+    for (int32_t i = 0; i < nsys; ++i) {
+        stats[4 * i + 0] = 0; stats[4 * i + 1] = 0; stats[4 * i + 2] = INFINITY; stats[4 * i + 3] = 0;
+    }
+    c.err = cudaMemcpyAsync(dseg, hseg.data(), 8 * (nsys + 1), cudaMemcpyHostToDevice, c.s);
+    if (!c.err) c.err = cudaMemsetAsync(dstate, 0, 4 * nsys, c.s);   // the <b, b> pass below reads it
+    if (!c.err) c.err = cudaStreamSynchronize(c.s);                   // hseg lives on the host
+    c.zero(dev_x);
+    c.smax = 2;
+    {
+        Fused f{};
+        f.op = 0; f.ic0 = f.ic1 = -1; f.nq = 1; f.qa[0] = dev_b; f.qb[0] = dev_b;
+        c.fused(f);
+        c.fin(1, S_GEN0, 0, 0, FIN_B_INIT);
+    }
+    c.copy(r, dev_b);
+    c.copy(rh, dev_b);
+    c.zero(pv);
+    c.zero(v);
+    const double *M_p = precond ? ph : pv;
+    const double *M_s = precond ? sh : sv;
+    std::vector<int> hstate(nsys);
+    auto all_stopped = [&]() {
+        if (c.err) return true;
+        c.err = cudaMemcpyAsync(hstate.data(), dstate, 4 * nsys, cudaMemcpyDeviceToHost, c.s);
+        if (!c.err) c.err = cudaStreamSynchronize(c.s);
+        if (c.err) return true;
+        for (int x : hstate)
+            if (x != 2) return false;
+        return true;
+    };
+    for (int64_t it = 1; it <= max_iters && !all_stopped(); ++it) {
+        c.it = it;
+        c.smax = 0;
+        Fused f{};   // p = r + beta (p - omega v)
+        f.op = 2; f.u = pv; f.v = v; f.x = r; f.ic0 = S_BETA; f.ic1 = S_OMEGA; f.sgn0 = 1.0; f.nq = 0;
+        c.fused(f);
+        if (precond && c.apply(pv, ph) != BILUK_OK) return krylov_fail(c, "bicgstab_batched");
+        c.spmv(M_p, v);
+        Fused fv{};   // <r^, v> -> alpha
+        fv.op = 0; fv.ic0 = fv.ic1 = -1; fv.nq = 1; fv.qa[0] = rh; fv.qb[0] = v;
+        c.fused(fv);
+        c.fin(1, S_RV, 0, 0, FIN_B_ALPHA);
+        Fused fs{};   // s = r - alpha v ; ||s||^2 -> half-step test
+        fs.op = 1; fs.u = sv; fs.x = r; fs.v = v; fs.ic0 = S_ALPHA; fs.ic1 = -1; fs.sgn0 = -1.0; fs.nq = 1;
+        c.fused(fs);
+        c.fin(1, S_SS, 0, 0, FIN_B_HALF);
+        if (precond && c.apply(sv, sh) != BILUK_OK) return krylov_fail(c, "bicgstab_batched");
+        c.spmv(M_s, t);
+        Fused fd{};   // <t, t>, <t, s> -> omega
+        fd.op = 0; fd.ic0 = fd.ic1 = -1; fd.nq = 2; fd.qa[0] = t; fd.qb[0] = t; fd.qa[1] = t; fd.qb[1] = sv;
+        c.fused(fd);
+        c.fin(2, S_TT, S_TS, 0, FIN_B_OMEGA);
+        c.smax = 1;   // x += xa p^ + xw s^  (also for systems finishing at the half step)
+        Fused fx{};
+        fx.op = 3; fx.u = dev_x; fx.v = M_p; fx.w = M_s; fx.ic0 = S_XA; fx.ic1 = S_XW; fx.sgn0 = 1.0;
+        c.fused(fx);
+        c.smax = 0;   // r = s - omega t ; ||r||^2 ; rho_next = <r^, r>
+        Fused fr{};
+        fr.op = 1; fr.u = r; fr.x = sv; fr.v = t; fr.ic0 = S_OMEGA; fr.ic1 = -1; fr.sgn0 = -1.0; fr.nq = 2;
+        fr.qa[0] = nullptr; fr.qb[0] = nullptr; fr.qa[1] = rh; fr.qb[1] = nullptr;
+        c.fused(fr);
+        c.fin(2, S_RR, S_RHO_NEXT, 0, FIN_B_BETA);
+    }
+    if (c.err) return krylov_fail(c, "bicgstab_batched");
+    // true residuals ||b_s - A_s x_s|| / ||b_s||
+    c.spmv(dev_x, t);
+    if (!c.err) {
+        sub_kernel<<<c.sms() * 8, 256, 0, c.s>>>(t, dev_b, t, len);
+        c.err = cudaGetLastError();
+    }
+    c.smax = 2;
+    {
+        Fused f{};
+        f.op = 0; f.ic0 = f.ic1 = -1; f.nq = 1; f.qa[0] = t; f.qb[0] = t;
+        c.fused(f);
+        c.fin(1, S_GEN1, 0, 0, FIN_B_TRUE);
+    }
+    std::vector<double> hs(size_t(B_STRIDE) * nsys);
+    if (!c.err) c.err = cudaMemcpyAsync(hs.data(), scal, 8 * hs.size(), cudaMemcpyDeviceToHost, c.s);
+    if (!c.err) c.err = cudaStreamSynchronize(c.s);
+    if (c.err) return krylov_fail(c, "bicgstab_batched");
+    for (int32_t i = 0; i < nsys; ++i) {
+        const double *q = hs.data() + size_t(B_STRIDE) * i;
+        stats[4 * i + 0] = q[S_ITS];
+        stats[4 * i + 1] = q[S_TRUE] <= rel_tol ? 1 : 0;
+        stats[4 * i + 2] = q[S_TRUE];
+        stats[4 * i + 3] = q[S_NH];
+    }
     return M ? biluk_plan_status(M, stream) : BILUK_OK;
 }
 

@@ -24,7 +24,7 @@ import numpy as np
 from . import _native as nat
 from .device import alloc_bytes, enter, operator_for, to_device_f64, torch
 
-__all__ = ["SolverConfig", "SolveStats", "gmres", "bicgstab"]
+__all__ = ["SolverConfig", "SolveStats", "gmres", "bicgstab", "bicgstab_batched"]
 
 _RHS_MODES = ("ones-solution", "given")
 
@@ -162,3 +162,74 @@ def bicgstab(a, b, M=None, cfg=None, workers=1):
     """
     cfg = SolverConfig() if cfg is None else cfg
     return _solve("bicgstab", a, b, M, cfg, 0)
+
+
+def bicgstab_batched(a, b, segments=None, M=None, cfg=None):
+    """BiCGSTAB over independent systems packed as one block-diagonal matrix.
+
+    ``a`` is the batch operator (e.g. ``sparse.block_diagonal(mats)``), ``M``
+    its preconditioner (``build_preconditioner(a, k)`` -- ILU(k) decouples over
+    the diagonal blocks), ``segments`` the block-row offsets of the systems
+    (``[0, n_0, n_0 + n_1, ..., n]``; default ``a.batch_segments``, which
+    ``block_diagonal`` sets; explicit segments are checked not to couple).
+    Each system iterates as :func:`bicgstab` would on it alone (its own
+    scalars and stopping tests; the result is the single solve's up to the
+    preconditioner's rounding) while every SpMV and preconditioner apply covers
+    the whole batch in one launch.  Returns ``(x, [SolveStats per
+    system])``; ``x`` is numpy unless ``b`` is a CUDA tensor.  Residual
+    histories are not kept.
+    """
+    cfg = SolverConfig() if cfg is None else cfg
+    t0 = perf_counter()
+    t = torch()
+    trusted = segments is None   # block_diagonal output: no coupling by construction
+    if trusted:
+        segments = getattr(a, "batch_segments", None)
+        if segments is None:
+            raise ValueError("segments required (the matrix does not come from block_diagonal)")
+    seg = np.ascontiguousarray(np.asarray(segments, dtype=np.int64))
+    if seg.ndim != 1 or seg.size < 2:
+        raise ValueError("segments must hold at least two offsets")
+    op = operator_for(a)
+    if op.n != op.ncols:
+        raise ValueError("bicgstab requires a square matrix")
+    if seg[0] != 0 or seg[-1] != op.n or np.any(np.diff(seg) < 0):
+        raise ValueError("segments must be non-decreasing offsets from 0 to n")
+    rp = getattr(a, "row_ptr", None) if not trusted else None
+    if rp is not None:   # the systems must not couple: every entry stays inside its row's segment
+        rp = np.asarray(rp, dtype=np.int64)
+        ci = np.asarray(a.col_idx, dtype=np.int64)
+        rows = np.repeat(np.arange(rp.size - 1, dtype=np.int64), np.diff(rp))
+        if np.any(np.searchsorted(seg, rows, side="right") != np.searchsorted(seg, ci, side="right")):
+            raise ValueError("matrix couples two batch systems (not block diagonal over segments)")
+    length = op.n * op.bs
+    on_device = isinstance(b, t.Tensor) and b.is_cuda
+    if not on_device:
+        b = np.asarray(b, dtype=np.float64)
+        if b.shape != (length,):
+            raise ValueError(f"right-hand side length {b.shape} does not match n={length}")
+    elif b.numel() != length:
+        raise ValueError(f"right-hand side length {tuple(b.shape)} does not match n={length}")
+    plan, cb, keep = _precond_args(M, length)
+    stream = enter()
+    bd = to_device_f64(b)
+    x = t.empty(length, dtype=t.float64, device="cuda")
+    L = nat.lib()
+    nsys = seg.size - 1
+    work, workp = alloc_bytes(L.biluk_krylov_batched_workspace_bytes(length, nsys))
+    stats = (ctypes.c_double * (4 * nsys))()
+    rc = L.biluk_bicgstab_batched(op.handle, plan, cb, None, nsys, seg.ctypes.data_as(nat.P_i64), bd.data_ptr(),
+                                  x.data_ptr(), workp, int(cfg.max_iters), float(cfg.rel_tol), stats, stream)
+    del keep
+    nat.check(rc, stage="bicgstab_batched")
+    out = x if on_device else x.cpu().numpy()
+    dt = perf_counter() - t0
+    res = []
+    for i in range(nsys):
+        st = SolveStats()
+        st.iterations = int(stats[4 * i])
+        st.converged = bool(stats[4 * i + 1])
+        st.final_relative_residual = float(stats[4 * i + 2])
+        st.solve_seconds = dt
+        res.append(st)
+    return out, res

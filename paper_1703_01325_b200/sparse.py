@@ -291,7 +291,8 @@ def block_diagonal(mats):
     of its own system), so factoring and applying the batch as one operator
     equals factoring and applying every system alone -- while one persistent
     sweep interleaves their level chains.  Vectors of the batch are the
-    systems' vectors concatenated in order.
+    systems' vectors concatenated in order; ``batch_segments`` holds the
+    systems' block-row offsets (what ``bicgstab_batched`` takes).
     """
     parts = [as_bsr(m) for m in mats]   # (bs, n_rows, n_cols, row_ptr, col_idx, values)
     if not parts:
@@ -314,4 +315,7 @@ def block_diagonal(mats):
         vals[z * bs * bs:(z + nz) * bs * bs] = qv.reshape(-1)
         r += nb
         z += nz
-    return BcsrMatrix(bs, n_tot, n_tot, rp, ci, vals)
+    out = BcsrMatrix(bs, n_tot, n_tot, rp, ci, vals)
+    # block-row offsets of the systems; block diagonal by construction
+    out.batch_segments = np.concatenate([[0], np.cumsum([q[1] for q in parts])]).astype(np.int64)
+    return out

@@ -231,3 +231,46 @@ def test_block_diagonal_batch_equals_independent_systems(b2, k):
         want = orc.build_preconditioner(n, bs, rp, ci, vals, k).apply(r)
         assert rel_err(z[off:off + n * bs], want) <= TOL
         off += n * bs
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_batched_bicgstab_equals_independent_solves(b2, k):
+    """Batched BiCGSTAB: each system iterates as if alone (same x, same count) and
+    its count is within +-1 of the oracle's; a zero right-hand side stops at once."""
+    shapes = [(7, 6, 5), (9, 4, 6), (5, 5, 5), (8, 7, 3)]
+    mats, rhs = [], []
+    for s, (nx, ny, nz) in enumerate(shapes):
+        n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, ny, nz, 3, seed=40 + s)
+        mats.append(b2.BcsrMatrix(bs, n, n, rp, ci, vals))
+        r = np.random.default_rng(s).standard_normal(n * bs)
+        rhs.append(np.zeros_like(r) if s == 2 else r)
+    big = b2.block_diagonal(mats)
+    seg = np.concatenate([[0], np.cumsum([m.num_block_rows for m in mats])])
+    cfg = b2.SolverConfig(rel_tol=1e-9)
+    assert np.array_equal(big.batch_segments, seg)
+    xb, stats = b2.bicgstab_batched(big, np.concatenate(rhs), M=b2.build_preconditioner(big, k), cfg=cfg)
+    assert len(stats) == len(mats)
+    for i, (m, r) in enumerate(zip(mats, rhs)):
+        xs, st = b2.bicgstab(m, r, M=b2.build_preconditioner(m, k), cfg=cfg)
+        part = xb[seg[i] * 3:seg[i + 1] * 3]
+        assert stats[i].converged == st.converged
+        if i == 2:
+            assert stats[i].iterations == 0 and stats[i].converged and not np.any(part)
+            continue
+        # the batch's sweep sums may round differently from the single system's
+        # (record layout), so x agrees to rounding -- or to the tolerance when
+        # that rounding moves the stopping test by one iteration
+        assert abs(stats[i].iterations - st.iterations) <= 1
+        assert rel_err(part, xs) <= (1e-10 if stats[i].iterations == st.iterations else 1e-6)
+        n, bs = m.num_block_rows, 3
+        f = orc.build_preconditioner(n, bs, m.row_ptr, m.col_idx, m.values, k)
+        _, its, conv, _, _ = orc.bicgstab(lambda v: orc.bsr_spmv(n, bs, m.row_ptr, m.col_idx, m.values, v), r,
+                                          precond=f.apply, rel_tol=1e-9)
+        assert conv and abs(its - stats[i].iterations) <= 1
+
+
+def test_batched_bicgstab_rejects_coupled_segments(b2):
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(6, 5, 4, 3, seed=3)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    with pytest.raises(ValueError):
+        b2.bicgstab_batched(a, np.ones(n * bs), [0, n // 2, n])

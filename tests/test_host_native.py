@@ -214,6 +214,7 @@ def test_block_diagonal_batch_assembly():
     ms = [b2.reservoir_block_grid(3 + s, 3, 2, 2, seed=s) for s in range(3)]
     big = b2.block_diagonal([b2.BcsrMatrix(bs, n, n, rp, ci, v) for n, bs, rp, ci, v in ms])
     assert big.shape == (sum(n for n, *_ in ms) * 2,) * 2
+    assert big.batch_segments.tolist() == [0, ms[0][0], ms[0][0] + ms[1][0], sum(n for n, *_ in ms)]
     r = z = 0
     for n, bs, rp, ci, v in ms:
         assert np.array_equal(big.row_ptr[r:r + n + 1] - big.row_ptr[r], rp)
@@ -222,8 +223,7 @@ def test_block_diagonal_batch_assembly():
         r += n
         z += rp[-1]
     # the symbolic phase of the batch is the per-system patterns, shifted
-    pb = b2.symbolic_phase(b2.extract_point_pattern(big) if False else b2.PatternMatrix.from_csr_arrays(
-        big.num_block_rows, big.row_ptr, big.col_idx), 1)
+    pb = b2.symbolic_phase(b2.PatternMatrix.from_csr_arrays(big.num_block_rows, big.row_ptr, big.col_idx), 1)
     rb, cb = pb.to_csr_arrays()
     r = z = 0
     for n, bs, rp, ci, v in ms:
