@@ -342,6 +342,10 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             const int s = i % K;
             const uint32_t ph = uint32_t(i / K) & 1u;
             if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) break;
+            // clock64 stamps of the stages for the first 16384 records (trace debug rows)
+            unsigned long long *dbg =
+                (a.trace && gt == 0 && r0 + i < 16384) ? a.trace + size_t(a.nrec_total + r0 + i) * 8 : nullptr;
+            if (dbg) dbg[0] = clock64();
             const unsigned char *rec = dring + slot_off[s];
             const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
             const int nr = h.nrows, S = h.S, ng = h.nglob;
@@ -446,10 +450,13 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                 idx2 = iarr[q2];
                 init_acc(q2, acc2);
             }
+            if (dbg) dbg[1] = clock64();
             if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
             if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 4] = globaltimer();
+            if (dbg) dbg[2] = clock64();
             // the other group has published record i-1
             if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
+            if (dbg) dbg[3] = clock64();
             if (live) {
                 // register-staged slots: every dependency load first, then the
                 // products, summed as a tree and subtracted once
@@ -477,7 +484,9 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
 #pragma unroll
                 for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
                 smem_slots(gt, SR, acc);
+                if (dbg) dbg[4] = clock64();
                 publish(gt, idx, acc);
+                if (dbg) dbg[5] = clock64();
             }
             if (nr > n1) {
                 // the record's second level: its dependencies on the first level
@@ -492,7 +501,9 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             // (an L record's y_u stores are read later by the async proxy)
             if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % PS_NGRP, 2 * PS_NG);
             if (!up) fence_proxy_async_global();
+            if (dbg) dbg[6] = clock64();
             mbar_arrive(empty_bar + s);
+            if (dbg) dbg[7] = clock64();
             if (a.trace && gt == 0) {
                 a.trace[size_t(r0 + i) * 8 + 5] = globaltimer();
                 uint32_t smid;

@@ -3,8 +3,12 @@
     python tools/trace_psweep.py --nx 128 --k 0 --out gpurun_out/ptrace_k0.npz
 
 Stamps per record (globaltimer ns, csrc/psweep.cu): 0 bulk copy issued,
-1 bytes seen landed (gather stage), 2 inputs gather issued, 3 dependencies
-ready (poll retired), 4 compute start, 5 compute end, 6 (cta << 32 | smid).
+1 landed (seen by the poll warp), 3 dependencies ready (poll retired),
+4 compute start (before the hand-over barrier), 5 compute end,
+6 (cta << 32 | smid), 7 flags.  The debug rows after the records hold, for the
+first 16384 records, clock64 stamps of the compute group's stages (thread 0):
+landed, prepared, dependencies waited, hand-over, products, published,
+arrive + fence, released.
 """
 
 import argparse
@@ -22,9 +26,8 @@ def summarize(tr):
     t = (tr[:, :6] - t0) / 1e3   # us
     out = {"span_us": float(t[:, 5].max()), "records": int(tr.shape[0])}
     out["stage_us_median"] = {
-        "issue->landed": float(np.median(t[:, 1] - t[:, 0])),
-        "landed->gathered": float(np.median(t[:, 2] - t[:, 1])),
-        "gathered->deps_ready": float(np.median(t[:, 3] - t[:, 2])),
+        "issue->poll_start": float(np.median(t[:, 1] - t[:, 0])),
+        "poll": float(np.median(t[:, 3] - t[:, 1])),
         "deps_ready->compute_start": float(np.median(t[:, 4] - t[:, 3])),
         "compute": float(np.median(t[:, 5] - t[:, 4])),
     }
@@ -38,11 +41,22 @@ def summarize(tr):
         gaps.append(np.diff(tc[:, 5]))
         busy.append(tc[:, 5] - tc[:, 4])
     g = np.concatenate(gaps)
+    # is the hand-over chain waiting for the next group (start after the previous record's end)?
+    late = np.concatenate([t[np.where(cta == c)[0]][1:, 4] - t[np.where(cta == c)[0]][:-1, 5] for c in np.unique(cta)])
+    out["start_after_prev_end_us_median"] = float(np.median(late))
     out["cta_record_interval_us"] = {"median": float(np.median(g)), "mean": float(g.mean()),
                                      "p90": float(np.percentile(g, 90))}
     out["cta_first_start_us"] = {"min": float(min(first)), "median": float(np.median(first)), "max": float(max(first))}
     out["cta_last_end_us"] = {"min": float(min(last)), "median": float(np.median(last)), "max": float(max(last))}
     return out
+
+
+def stages(dbg):
+    """Median cycles of the compute group's stages (debug rows)."""
+    d = dbg[dbg[:, 0] > 0].astype(np.int64)
+    names = ["prep", "dep_wait", "handover", "products", "publish", "arrive_fence", "release"]
+    dd = np.diff(d, axis=1)
+    return {nm: float(np.median(dd[:, j][(dd[:, j] >= 0) & (dd[:, j] < 10**6)])) for j, nm in enumerate(names)}
 
 
 def main():
@@ -67,12 +81,13 @@ def main():
         b2.apply_preconditioner(f, rhs, out=out)
     torch.cuda.synchronize()
     f.status()
-    h = tr.cpu().numpy().astype(np.int64)[: f.info["records"]]
-    np.save((args.out or "/tmp/x.npz")[:-4] + "_dbg.npy", tr.cpu().numpy()[f.info["records"]:])
+    full = tr.cpu().numpy().astype(np.int64)
+    h, dbg = full[: f.info["records"]], full[f.info["records"]:]
     s = summarize(h)
+    s["compute_stage_cycles_median"] = stages(dbg)
     print(s, flush=True)
     if args.out:
-        np.savez_compressed(args.out, trace=h, info=np.array([f.info[k] for k in f.info]),
+        np.savez_compressed(args.out, trace=h, dbg=dbg, info=np.array([f.info[k] for k in f.info]),
                             keys=np.array(list(f.info)))
 
 
