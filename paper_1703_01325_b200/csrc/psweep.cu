@@ -36,7 +36,10 @@ constexpr int PS_NG = 128;            // threads per compute group (= rows per r
 constexpr int PS_NGRP = 2;            // compute groups (round-robin over records)
 constexpr int PS_NT = PS_NGRP * PS_NG; // compute threads
 constexpr int PS_NW = PS_NT / 32;     // compute warps; then producer, gather, poll warps
-constexpr int PS_NPOLL = 2;           // poll warps (alternate records)
+#ifndef PS_GPOLL
+#define PS_GPOLL 1                    // 1: each compute group fetches its records' dependencies itself
+#endif
+constexpr int PS_NPOLL = PS_GPOLL ? 0 : 2;   // poll warps (alternate records)
 constexpr int PS_NAUX = 2 + PS_NPOLL; // two producers (even / odd records) + poll warps
 constexpr int PS_PF = 16;             // records prefetched into L2 ahead of their bulk copy
 
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
     constexpr int VS = ps_vec_stride(BS);
     constexpr int K = PS_KSLOTS;
     constexpr int EPL = ps_glob_cap(BS) / 32;   // dependency entries per poll lane
-    static_assert(K % PS_NPOLL == 0, "poll warps must own whole ring slots");
+    static_assert(PS_NPOLL == 0 || K % PS_NPOLL == 0, "poll warps must own whole ring slots");
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[K];    // record bytes + inputs landed (two bulk copies)
     __shared__ __align__(8) uint64_t dep_bar[K];     // dependencies fetched (poll warp)
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
         }
         // never leave the CTA with copies in flight into its shared memory
         for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + (pp + 2 * g) % K, uint32_t((pp + 2 * g) / K) & 1u);
+#if !PS_GPOLL
     } else if (warp > PS_NW + 1) {
         // ============ poll: dependencies outside the on-chip ring ==============
         // warp p owns records p, p + NPOLL, ...; all its loads of a round are
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             }
             if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
         }
+#endif
     } else {
         // ========================= compute warps ==============================
         // two groups of PS_NG threads take alternate records (ping-pong).  A
@@ -359,6 +364,15 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             const double *vals = vbase + gt;
             const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off);
             const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
+#if PS_GPOLL
+            // dependencies outside the ring: thread e fetches entry e (tag-polled);
+            // the first load is issued here so its round trip overlaps the prep
+            const int32_t *gpos = desc + size_t(S) * nr;
+            const double *gvec = up ? a.x_t : a.y_t;
+            const bool dneed = gt < ng;
+            double dval[BS];
+            if (dneed) ld_row<BS>(gvec + size_t(gpos[gt]) * VS, dval);
+#endif
             // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
             auto init_acc = [&](int q, double (&acc)[BS]) {
                 const double *inp = inp0 + size_t(q) * VS;
@@ -451,12 +465,46 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                 init_acc(q2, acc2);
             }
             if (dbg) dbg[1] = clock64();
+#if PS_GPOLL
+            {
+                auto fetch_dep = [&](int e, double (&dv)[BS], bool loaded) {
+                    const double *src = gvec + size_t(gpos[e]) * VS;
+                    if (!loaded) ld_row<BS>(src, dv);
+                    uint64_t t0 = 0;
+                    uint32_t spins = 0;
+                    while (true) {
+                        uint32_t ok = 1;
+#pragma unroll
+                        for (int q = 0; q < BS; ++q) ok &= (tag_of(dv[q]) == par);
+                        if (ok) break;
+                        if (ps_timed_out(t0, spins, a)) {
+                            abort_flag = 1;
+                            break;
+                        }
+                        ld_row<BS>(src, dv);
+                    }
+#pragma unroll
+                    for (int q = 0; q < BS; ++q) sts(dep_s + uint32_t(q * ng + e) * 8u, untag(dv[q]));
+                };
+                if (dneed) fetch_dep(gt, dval, true);
+                for (int e = gt + PS_NG; e < ng; e += PS_NG) {
+                    double dv2[BS];
+                    fetch_dep(e, dv2, false);
+                }
+                if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
+                if (i == 0) named_bar_sync(3 + grp, PS_NG);   // the fetched values, to the whole group
+            }
+#else
             if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
+#endif
             if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 4] = globaltimer();
             if (dbg) dbg[2] = clock64();
             // the other group has published record i-1
             if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
             if (dbg) dbg[3] = clock64();
+#if PS_GPOLL
+            if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
+#endif
             if (live) {
                 // register-staged slots: every dependency load first, then the
                 // products, summed as a tree and subtracted once
