@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                     fetch_dep(e, dv2, false);
                 }
                 if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
-                if (i == 0) named_bar_sync(3 + grp, PS_NG);   // the fetched values, to the whole group
+                if (i == 0) named_bar_sync(1 + PS_NGRP + grp, PS_NG);   // the fetched values, to the whole group
             }
 #else
             if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             if (nr > n1) {
                 // the record's second level: its dependencies on the first level
                 // are in the ring once the group has passed this barrier
-                named_bar_sync(3 + grp, PS_NG);
+                named_bar_sync(1 + PS_NGRP + grp, PS_NG);
                 if (live2) {
                     smem_slots(q2, 0, acc2);
                     publish(q2, idx2, acc2);
