@@ -109,6 +109,13 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
  * Asynchronous; a dependency-wait timeout is reported by biluk_plan_status. */
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream);
 
+/* Diagnostics: CUDA events around the sweep launch of every subsequent apply
+ * (on = 1; 0 removes them).  biluk_plan_sweep_ms waits for the last apply's
+ * sweep and returns its duration -- the sweep kernel alone, without the
+ * right-hand-side permutation launched before it. */
+int biluk_plan_set_timing(biluk_plan_t *plan, int32_t on);
+int biluk_plan_sweep_ms(biluk_plan_t *plan, float *ms);
+
 /* Runtime knobs of the sweep kernel (no effect on results):
  *   "gap"             fine-grained dependency polling starts when every level
  *                     <= (tile level - gap) is complete (default 2)

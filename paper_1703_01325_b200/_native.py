@@ -50,6 +50,8 @@ _SIGS = {
     "biluk_plan_tune": (ctypes.c_int, [c_vp, ctypes.c_char_p, c_i64]),
     "biluk_plan_set_trace": (ctypes.c_int, [c_vp, c_vp]),
     "biluk_plan_tile_levels": (ctypes.c_int, [c_vp, c_vp]),
+    "biluk_plan_set_timing": (ctypes.c_int, [c_vp, c_i32]),
+    "biluk_plan_sweep_ms": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_float)]),
     "biluk_plan_records": (ctypes.c_int, [c_vp, c_vp, c_i64]),
     "biluk_plan_info": (ctypes.c_int, [c_vp, P_i64, c_i32]),
     "biluk_plan_copy_factors": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -131,17 +131,21 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     } else {
         cudaGetLastError();   // no device here: plan for a B200
     }
-    // apply engine: the partitioned sweep; the tiled level-order sweep only
-    // for patterns the partitioned one cannot stage (very long block rows)
-    // measured on B200 (tools/engine_compare.py): the
-    // partitioned sweep wins for ILU(0) with small blocks; with fill (longer
-    // rows, 2-4x the levels) or bs > 4 the tiled level-order sweep is faster
+    // apply engine, from B200 measurements (tools/engine_compare.py, DESIGN.md
+    // §3): the partitioned sweep wins while its records per part stay few --
+    // ILU(0) with b <= 3; ILU(1) with b <= 3 up to ~400 records per part
+    // (100^3 yes, 128^3 no); ILU(0) with b = 4 up to ~200 (64^3 yes, 100^3
+    // no).  More fill (longer rows, more levels), larger blocks or batches of
+    // many systems go to the tiled level-order sweep.  BILUK_ENGINE overrides.
     Plan &P = h->p;
-    P.engine = (k == 0 && bs <= 4) ? 1 : 0;
-    if (const char *env = std::getenv("BILUK_ENGINE")) P.engine = std::atoi(env) == 0 ? 0 : 1;
+    const char *env = std::getenv("BILUK_ENGINE");
+    P.engine = ((bs <= 3 && k <= 1) || (bs == 4 && k == 0)) ? 1 : 0;
+    if (env) P.engine = std::atoi(env) == 0 ? 0 : 1;
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
-        if (rc == BILUK_EUNSUPPORTED) {
+        const double per_part = P.ps.P > 0 ? double(P.ps.rec.size()) / P.ps.P : 0.0;
+        const double limit = bs <= 3 ? (k == 0 ? 1e30 : 400.0) : 200.0;
+        if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;
             P.ps = PSweep{};
         } else if (rc != BILUK_OK) {
@@ -278,7 +282,9 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
         a.b_perm = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
         a.y_u = reinterpret_cast<double *>(p.ws + p.off.ps_yu);
         CUDA_TRY(launch_permute_b(p, dev_b, static_cast<cudaStream_t>(stream)), "apply");
+        if (plan->tev[0]) CUDA_TRY(cudaEventRecord(plan->tev[0], static_cast<cudaStream_t>(stream)), "apply");
         CUDA_TRY(launch_psweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+        if (plan->tev[1]) CUDA_TRY(cudaEventRecord(plan->tev[1], static_cast<cudaStream_t>(stream)), "apply");
         return BILUK_OK;
     }
     SweepArgs a{};
@@ -310,7 +316,29 @@ int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, voi
     a.probe_sleep_ns = p.tune.probe_sleep_ns;
     a.trace = p.trace;
     a.trace_mode = p.tune.trace_mode;
+    if (plan->tev[0]) CUDA_TRY(cudaEventRecord(plan->tev[0], static_cast<cudaStream_t>(stream)), "apply");
     CUDA_TRY(launch_sweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+    if (plan->tev[1]) CUDA_TRY(cudaEventRecord(plan->tev[1], static_cast<cudaStream_t>(stream)), "apply");
+    return BILUK_OK;
+}
+
+int biluk_plan_set_timing(biluk_plan_t *plan, int32_t on) {
+    if (!plan) return fail(BILUK_EARG, "null plan");
+    for (cudaEvent_t &e : plan->tev) {
+        if (on && !e) CUDA_TRY(cudaEventCreate(&e), "set_timing");
+        if (!on && e) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
+    }
+    return BILUK_OK;
+}
+
+int biluk_plan_sweep_ms(biluk_plan_t *plan, float *ms) {
+    if (!plan || !ms) return fail(BILUK_EARG, "null argument");
+    if (!plan->tev[0]) return fail(BILUK_EARG, "timing is off (biluk_plan_set_timing)");
+    CUDA_TRY(cudaEventSynchronize(plan->tev[1]), "sweep_ms");
+    CUDA_TRY(cudaEventElapsedTime(ms, plan->tev[0], plan->tev[1]), "sweep_ms");
     return BILUK_OK;
 }
 

@@ -2,6 +2,8 @@
 // (kernels.cu) and the C ABI (abi.cu).  Not part of the public interface.
 #pragma once
 
+#include <cuda_runtime_api.h>
+
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -279,6 +281,12 @@ int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, c
 // the opaque handles of the C ABI
 struct biluk_plan {
     biluk::Plan p;
+    // optional CUDA events around the sweep launch (biluk_plan_set_timing)
+    cudaEvent_t tev[2] = {nullptr, nullptr};
+    ~biluk_plan() {
+        for (cudaEvent_t e : tev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 struct biluk_op {
     biluk::Op o;

@@ -112,6 +112,16 @@ class BlockIlukFactors:
         nat.check(nat.lib().biluk_plan_tile_levels(self._h, nat.ptr(out)))
         return out
 
+    def set_sweep_timing(self, enable=True):
+        """Diagnostics: CUDA events around the sweep launch of every later apply."""
+        nat.check(nat.lib().biluk_plan_set_timing(self._h, 1 if enable else 0))
+
+    def sweep_ms(self):
+        """Duration of the last apply's sweep kernel (waits for it); needs set_sweep_timing."""
+        ms = ctypes.c_float()
+        nat.check(nat.lib().biluk_plan_sweep_ms(self._h, ctypes.byref(ms)))
+        return float(ms.value)
+
     def set_trace(self, enable=True):
         """Diagnostics: record per-tile globaltimer stamps on later applies; returns the (T, 4) buffer."""
         if not enable:

@@ -274,3 +274,22 @@ def test_batched_bicgstab_rejects_coupled_segments(b2):
     a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
     with pytest.raises(ValueError):
         b2.bicgstab_batched(a, np.ones(n * bs), [0, n // 2, n])
+
+
+def test_sweep_timing_hooks(b2):
+    """biluk_plan_set_timing / sweep_ms: the sweep kernel alone, both engines."""
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(20, 18, 16, 3, seed=5)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    rhs = torch.randn(n * bs, dtype=torch.float64, device="cuda")
+    for k in (0, 2):
+        f = b2.build_preconditioner(a, k)
+        ref = b2.apply_preconditioner(f, rhs)
+        f.set_sweep_timing(True)
+        x = b2.apply_preconditioner(f, rhs)
+        ms = f.sweep_ms()
+        f.set_sweep_timing(False)
+        assert 0.0 < ms < 1000.0
+        assert torch.equal(x, ref)          # timing does not change the result
+        with pytest.raises(ValueError):
+            f.sweep_ms()                    # off again

@@ -1,6 +1,6 @@
 """Apply time of both sweep engines over the BASELINE configs (GPU).
 
-    python tools/engine_compare.py
+    python tools/engine_compare.py [NX_BS_K ...]      (default: the BASELINE configs)
 """
 import os
 import sys
@@ -15,10 +15,8 @@ CASES = [(16, 3, 0), (64, 3, 1), (128, 3, 0), (128, 3, 1), (128, 3, 2), (100, 4,
 def main():
     import torch
     import paper_1703_01325_b200 as b2
-    sel = sys.argv[1:]
-    for nx, bs, k in CASES:
-        if sel and f"{nx}_{bs}_{k}" not in sel:
-            continue
+    cases = [tuple(int(v) for v in c.split("_")) for c in sys.argv[1:]] or CASES
+    for nx, bs, k in cases:
         n, bs_, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, bs, seed=0)
         a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
         rhs = torch.from_numpy(np.random.default_rng(1).standard_normal(n * bs)).cuda()
