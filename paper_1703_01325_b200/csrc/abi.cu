@@ -133,10 +133,10 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     }
     // apply engine, from B200 measurements (tools/engine_compare.py, DESIGN.md
     // §3): the partitioned sweep wins while its records per part stay few --
-    // ILU(0) with b <= 3; ILU(1) with b <= 3 up to ~400 records per part
-    // (100^3 yes, 128^3 no); ILU(0) with b = 4 up to ~200 (64^3 yes, 100^3
-    // no).  More fill (longer rows, more levels), larger blocks or batches of
-    // many systems go to the tiled level-order sweep.  BILUK_ENGINE overrides.
+    // ILU(0) with b <= 3; ILU(1) with b <= 3 and ILU(0) with b = 4 up to ~400
+    // records per part (100^3 yes, 128^3 ILU(1) no).  More fill (longer rows,
+    // more levels), larger blocks or batches of many systems go to the tiled
+    // level-order sweep.  BILUK_ENGINE overrides.
     Plan &P = h->p;
     const char *env = std::getenv("BILUK_ENGINE");
     P.engine = ((bs <= 3 && k <= 1) || (bs == 4 && k == 0)) ? 1 : 0;
@@ -144,7 +144,10 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
         const double per_part = P.ps.P > 0 ? double(P.ps.rec.size()) / P.ps.P : 0.0;
-        const double limit = bs <= 3 ? (k == 0 ? 1e30 : 400.0) : 200.0;
+        const double limit = (bs <= 3 && k == 0) ? 1e30 : 400.0;
+        // three compute groups (blocks read at the products) measured faster
+        // for ILU(0); two (blocks staged in registers) for ILU(1)
+        P.ps.groups = k == 0 ? 3 : 2;
         if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;
             P.ps = PSweep{};

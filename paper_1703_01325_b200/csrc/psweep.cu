@@ -33,9 +33,10 @@ using namespace dev;
 namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
-constexpr int PS_NGRP = 2;            // compute groups (round-robin over records)
-constexpr int PS_NT = PS_NGRP * PS_NG; // compute threads
-constexpr int PS_NW = PS_NT / 32;     // compute warps; then producer, gather, poll warps
+// compute groups (round-robin over records) are a template parameter G: 2 or 3
+#ifndef PS_EARLY_HANDOVER
+#define PS_EARLY_HANDOVER 0           // 1: hand over after the ring stores, global stores after it
+#endif
 #ifndef PS_GPOLL
 #define PS_GPOLL 1                    // 1: each compute group fetches its records' dependencies itself
 #endif
@@ -137,8 +138,9 @@ __device__ __forceinline__ bool mbar_wait_or_abort(uint64_t *bar, uint32_t phase
     return true;
 }
 
-template <int BS>
-__global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const PSweepArgs a) {
+template <int BS, int G>
+__global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(const PSweepArgs a) {
+    constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the producers (and poll warps)
     constexpr int BS2 = BS * BS;
     constexpr int VS = ps_vec_stride(BS);
     constexpr int K = PS_KSLOTS;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
         const uint32_t vring_s = 0;   // the vector ring starts the dynamic shared memory
         auto lds = [&](uint32_t off) -> double { return *reinterpret_cast<const double *>(smem + off); };
         auto sts = [&](uint32_t off, double v) { *reinterpret_cast<double *>(smem + off) = v; };
-        for (int i = grp; i < nrec; i += PS_NGRP) {
+        for (int i = grp; i < nrec; i += G) {
             const int s = i % K;
             const uint32_t ph = uint32_t(i / K) & 1u;
             if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) break;
@@ -424,10 +426,15 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
             };
             // publish row q: ring (this part), tagged global vector (other parts),
             // and y for this part's U' sweep (L) / the caller's x (U')
-            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
+            // publish row q in two steps: the ring (this part's next levels --
+            // the only thing the hand-over waits for), then, after the hand-over,
+            // the tagged global vector (other parts) and y_u (L) / the caller's x (U')
+            auto publish_ring = [&](int q, const double (&acc)[BS]) {
                 const uint32_t rs = vring_s + uint32_t((h.seq0 + q) & a.ring_mask) * 8u;
 #pragma unroll
                 for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
+            };
+            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
                 double pub[BS];
 #pragma unroll
                 for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
@@ -444,7 +451,14 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                 }
             };
             double acc[BS], acc2[BS];
-            double v[SR][BS2];
+            // staged slots: all SR with two groups; with three the registers
+            // go to the third group and the blocks are read at the products
+            constexpr int SV = G == 2 ? SR : 0;
+            double v[SV > 0 ? SV : 1][BS2];
+            // element e of slot u's block of this thread's row (registers, or shared memory)
+            auto vblk = [&](int u, int e) -> double {
+                return u < SV ? v[u][e] : (u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0);
+            };
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
             uint32_t xs[SR];   // its component stride in bytes
             int idx = 0, idx2 = 0;   // L: the row's U' position; U': its natural row
@@ -457,7 +471,8 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                     xa[u] = d >= 0 ? vring_s + uint32_t(d) * 8u : dep_s + uint32_t(-d - 1) * 8u;
                     xs[u] = d >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
 #pragma unroll
-                    for (int e = 0; e < BS2; ++e) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
+                    for (int e = 0; e < BS2; ++e)
+                        if (u < SV) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
                 }
             }
             if (live2) {
@@ -492,7 +507,7 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                     fetch_dep(e, dv2, false);
                 }
                 if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
-                if (i == 0) named_bar_sync(1 + PS_NGRP + grp, PS_NG);   // the fetched values, to the whole group
+                if (i == 0) named_bar_sync(1 + G + grp, PS_NG);   // the fetched values, to the whole group
             }
 #else
             if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
@@ -517,11 +532,11 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
 #pragma unroll
                 for (int u = 0; u < SR; ++u) {
 #pragma unroll
-                    for (int r = 0; r < BS; ++r) pr[u][r] = v[u][r] * x[u][0];
+                    for (int r = 0; r < BS; ++r) pr[u][r] = vblk(u, r) * x[u][0];
 #pragma unroll
                     for (int c = 1; c < BS; ++c)
 #pragma unroll
-                        for (int r = 0; r < BS; ++r) pr[u][r] = fma(v[u][c * BS + r], x[u][c], pr[u][r]);
+                        for (int r = 0; r < BS; ++r) pr[u][r] = fma(vblk(u, c * BS + r), x[u][c], pr[u][r]);
                 }
 #pragma unroll
                 for (int w = 1; w < SR; w <<= 1)
@@ -533,21 +548,26 @@ __global__ void __launch_bounds__(PS_NT + 32 * PS_NAUX, 1) psweep_kernel(const P
                 for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
                 smem_slots(gt, SR, acc);
                 if (dbg) dbg[4] = clock64();
-                publish(gt, idx, acc);
+                publish_ring(gt, acc);
+                if (!PS_EARLY_HANDOVER) publish(gt, idx, acc);
                 if (dbg) dbg[5] = clock64();
             }
             if (nr > n1) {
                 // the record's second level: its dependencies on the first level
                 // are in the ring once the group has passed this barrier
-                named_bar_sync(1 + PS_NGRP + grp, PS_NG);
+                named_bar_sync(1 + G + grp, PS_NG);
                 if (live2) {
                     smem_slots(q2, 0, acc2);
-                    publish(q2, idx2, acc2);
+                    publish_ring(q2, acc2);
+                    if (!PS_EARLY_HANDOVER) publish(q2, idx2, acc2);
                 }
             }
-            // hand record i+1 to the other group, release record i's ring space
-            // (an L record's y_u stores are read later by the async proxy)
-            if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % PS_NGRP, 2 * PS_NG);
+            // hand record i+1 to the other group, then the global stores (off
+            // the chain), then release record i's ring space (an L record's y_u
+            // stores are read later by the async proxy)
+            if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % G, 2 * PS_NG);
+            if (PS_EARLY_HANDOVER && live) publish(gt, idx, acc);
+            if (PS_EARLY_HANDOVER && live2) publish(q2, idx2, acc2);
             if (!up) fence_proxy_async_global();
             if (dbg) dbg[6] = clock64();
             mbar_arrive(empty_bar + s);
@@ -691,10 +711,10 @@ cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s) {
 
 cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s) {
     const size_t smem = psweep_smem_bytes(p);
-    dim3 grid(p.ps.P), block(PS_NT + 32 * PS_NAUX);
+    dim3 grid(p.ps.P), block(p.ps.groups * PS_NG + 32 * PS_NAUX);
 #define PSWEEP_LAUNCH(BS)                                                                                  \
     {                                                                                                      \
-        auto kern = psweep_kernel<BS>;                                                                     \
+        auto kern = p.ps.groups == 3 ? psweep_kernel<BS, 3> : psweep_kernel<BS, 2>;                        \
         cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         if (e0 != cudaSuccess) return e0;                                                                  \
         void *args[] = {const_cast<PSweepArgs *>(&a)};                                                     \
@@ -710,10 +730,11 @@ cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm) {
     const size_t smem = psweep_smem_bytes(p);
 #define POCC(BS)                                                                                                  \
     {                                                                                                             \
-        auto kern = psweep_kernel<BS>;                                                                            \
+        auto kern = p.ps.groups == 3 ? psweep_kernel<BS, 3> : psweep_kernel<BS, 2>;                               \
         cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));      \
         if (e0 != cudaSuccess) return e0;                                                                         \
-        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, PS_NT + 32 * PS_NAUX, smem);                \
+        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, p.ps.groups * PS_NG + 32 * PS_NAUX, \
+                                                           smem);                                                 \
         if (e0 != cudaSuccess) return e0;                                                                         \
     }
     BILUK_BS_DISPATCH(p.bs, POCC)
