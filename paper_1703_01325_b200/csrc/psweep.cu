@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             // staged slots: all SR with two groups; with three the registers
             // go to the third group and the blocks are read at the products
             constexpr int SV = G == 2 ? SR : 0;
-            double v[SV > 0 ? SV : 1][BS2];
+            double v[SV > 0 ? SV : 1][BS2] = {};
             // element e of slot u's block of this thread's row (registers, or shared memory)
             auto vblk = [&](int u, int e) -> double {
                 return u < SV ? v[u][e] : (u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0);
