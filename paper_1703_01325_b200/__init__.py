@@ -12,8 +12,8 @@ from .factor import BlockIlukFactors, build_preconditioner, symbolic_phase
 from .krylov import SolverConfig, SolveStats, bicgstab, bicgstab_batched, gmres
 from .sparse import (BcsrMatrix, CsrMatrix, PatternMatrix, bcsr_from_csr, block_diagonal, csr_expand,
                      csr_from_triplets, extract_point_pattern)
-from .trisolve import (LevelSchedule, TriangularOperand, apply_preconditioner, build_level_schedule,
-                       strict_triangle)
+from .trisolve import (LevelSchedule, TriangularOperand, apply_preconditioner, apply_preconditioner_many,
+                       build_level_schedule, strict_triangle)
 from .device import DeviceOperator
 from .synthetic import reservoir_block_grid
 
@@ -34,7 +34,7 @@ def spmv(a, x, workers=1):
 __all__ = [
     "BcsrMatrix", "BlockIlukFactors", "CsrMatrix", "DeviceOperator", "FactorizationError", "LevelSchedule",
     "PatternMatrix", "SingularBlockError", "SolveStats", "SolverConfig", "StructuralError", "TriangularOperand",
-    "apply_preconditioner", "bcsr_from_csr", "bicgstab", "bicgstab_batched", "block_diagonal", "build_level_schedule", "build_preconditioner",
+    "apply_preconditioner", "apply_preconditioner_many", "bcsr_from_csr", "bicgstab", "bicgstab_batched", "block_diagonal", "build_level_schedule", "build_preconditioner",
     "csr_expand", "csr_from_triplets", "extract_point_pattern", "gmres", "reservoir_block_grid", "spmv",
     "strict_triangle", "symbolic_phase", "__version__",
 ]

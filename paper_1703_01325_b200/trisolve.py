@@ -24,7 +24,8 @@ from .device import enter, to_device_f64, torch
 from .errors import StructuralError
 from .sparse import CsrMatrix
 
-__all__ = ["TriangularOperand", "LevelSchedule", "strict_triangle", "build_level_schedule", "apply_preconditioner"]
+__all__ = ["TriangularOperand", "LevelSchedule", "strict_triangle", "build_level_schedule", "apply_preconditioner",
+           "apply_preconditioner_many"]
 
 
 class TriangularOperand:
@@ -120,3 +121,57 @@ def apply_preconditioner(f, b, workers=1, out=None):
     host = x.cpu().numpy()
     f.status()
     return host
+
+
+def apply_preconditioner_many(f, rhs, out=None):
+    """x_j = M^-1 b_j for k right-hand sides held in host memory, pipelined.
+
+    ``rhs`` is a (k, n*bs) float64 array (pinned torch CPU tensor or numpy;
+    numpy is staged once into pinned memory).  The copy in of b_{j+1} and the
+    copy out of x_{j-1} run on their own streams while the sweep of b_j runs,
+    so PCIe transfers in both directions overlap the device work; each x_j is
+    exactly ``apply_preconditioner(f, b_j)``.  Returns a (k, n*bs) pinned CPU
+    tensor (``out`` if given).
+    """
+    t = torch()
+    length = f.n * f.bs
+    if isinstance(rhs, t.Tensor):
+        if rhs.is_cuda:
+            raise ValueError("rhs must be in host memory (use apply_preconditioner for device tensors)")
+        host = rhs if (rhs.is_pinned() and rhs.dtype == t.float64 and rhs.is_contiguous()) else \
+            rhs.to(t.float64).contiguous().pin_memory()
+    else:
+        host = t.from_numpy(np.ascontiguousarray(rhs, dtype=np.float64)).pin_memory()
+    if host.dim() != 2 or host.shape[1] != length:
+        raise ValueError(f"right-hand sides {tuple(host.shape)} do not match (k, {length})")
+    k = host.shape[0]
+    res = out if out is not None else t.empty((k, length), dtype=t.float64).pin_memory()
+    if tuple(res.shape) != (k, length) or res.is_cuda:
+        raise ValueError("out must be a (k, n) host tensor")
+    enter()
+    comp = t.cuda.current_stream()
+    s_in, s_out = t.cuda.Stream(), t.cuda.Stream()
+    d_in = [t.empty(length, dtype=t.float64, device="cuda") for _ in range(2)]
+    d_out = [t.empty(length, dtype=t.float64, device="cuda") for _ in range(2)]
+    ev = {name: [t.cuda.Event() for _ in range(2)] for name in ("in_ready", "in_free", "out_ready", "out_free")}
+    for j in range(k):
+        u = j % 2
+        with t.cuda.stream(s_in):
+            if j >= 2:
+                s_in.wait_event(ev["in_free"][u])
+            d_in[u].copy_(host[j], non_blocking=True)
+            ev["in_ready"][u].record(s_in)
+        comp.wait_event(ev["in_ready"][u])
+        if j >= 2:
+            comp.wait_event(ev["out_free"][u])
+        nat.check(nat.lib().biluk_plan_apply(f.handle, d_in[u].data_ptr(), d_out[u].data_ptr(), comp.cuda_stream),
+                  stage="apply")
+        ev["in_free"][u].record(comp)
+        ev["out_ready"][u].record(comp)
+        with t.cuda.stream(s_out):
+            s_out.wait_event(ev["out_ready"][u])
+            res[j].copy_(d_out[u], non_blocking=True)
+            ev["out_free"][u].record(s_out)
+    s_out.synchronize()   # after it every copy and sweep above has completed
+    f.status()
+    return res

@@ -293,3 +293,21 @@ def test_sweep_timing_hooks(b2):
         assert torch.equal(x, ref)          # timing does not change the result
         with pytest.raises(ValueError):
             f.sweep_ms()                    # off again
+
+
+def test_apply_many_pipelined_equals_single_applies(b2):
+    """apply_preconditioner_many (host in/out, overlapped copies) == per-RHS applies, bitwise."""
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(14, 12, 10, 3, seed=8)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0)
+    rhs = np.random.default_rng(3).standard_normal((5, n * bs))
+    got = b2.apply_preconditioner_many(f, rhs)
+    assert tuple(got.shape) == (5, n * bs) and not got.is_cuda
+    for j in range(5):
+        assert np.array_equal(got[j].numpy(), b2.apply_preconditioner(f, rhs[j]))
+    one = b2.apply_preconditioner_many(f, torch.from_numpy(rhs[:1]).pin_memory())
+    assert np.array_equal(one[0].numpy(), got[0].numpy())
+    with pytest.raises(ValueError):
+        b2.apply_preconditioner_many(f, rhs[:, :-1])
+    with pytest.raises(ValueError):
+        b2.apply_preconditioner_many(f, torch.from_numpy(rhs).cuda())
