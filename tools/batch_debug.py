@@ -1,3 +1,10 @@
+"""Diagnostics: batched BiCGSTAB vs single solves per system, for each engine (GPU).
+
+    python tools/batch_debug.py
+
+Prints, per engine and k, each system's (batched iterations, single
+iterations, relative x difference, relative apply difference, engines).
+"""
 import os, sys, numpy as np
 sys.path.insert(0, os.getcwd())
 import paper_1703_01325_b200 as b2
