@@ -141,7 +141,7 @@ struct Sweep {                       // host copy of one sweep's tile layout
 // ---------------------------------------------------------------------------
 struct PRecHdr {        // 32 bytes
     int32_t nrows, S, nglob;
-    int32_t flags;      // bit 0: U' record; bits 1..: dependency level (diagnostics)
+    int32_t flags;      // bit 0: U' record; bits 1..9: rows; bits 10..: dependency level (diagnostics)
     int32_t seq0;       // ring sequence number of the first row
     int32_t pos0;       // vector position of the first row (y_t for L, x_t for U')
     int32_t vals_off;   // byte offset of dinv (U') / vals inside the record

@@ -34,9 +34,6 @@ namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
 // compute groups (round-robin over records) are a template parameter G: 2 or 3
-#ifndef PS_EARLY_HANDOVER
-#define PS_EARLY_HANDOVER 0           // 1: hand over after the ring stores, global stores after it
-#endif
 #ifndef PS_GPOLL
 #define PS_GPOLL 1                    // 1: each compute group fetches its records' dependencies itself
 #endif
@@ -357,9 +354,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
             const int nr = h.nrows, S = h.S, ng = h.nglob;
             const bool up = h.flags & 1;
-            const int n1 = (h.flags >> 1) & 0x1ff;   // rows of the record's first level; the rest are the next level
-            const int q2 = n1 + gt;                   // this thread's row of the second level
-            const bool live = gt < n1, live2 = q2 < nr;
+            const bool live = gt < nr;
             const int32_t *iarr = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr));
             const int32_t *desc = iarr + nr;
             const double *vbase = reinterpret_cast<const double *>(rec + h.vals_off) + (up ? size_t(BS2) * nr : 0);
@@ -426,15 +421,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             };
             // publish row q: ring (this part), tagged global vector (other parts),
             // and y for this part's U' sweep (L) / the caller's x (U')
-            // publish row q in two steps: the ring (this part's next levels --
-            // the only thing the hand-over waits for), then, after the hand-over,
-            // the tagged global vector (other parts) and y_u (L) / the caller's x (U')
-            auto publish_ring = [&](int q, const double (&acc)[BS]) {
+            // publish row q: the ring (this part's next levels), the tagged
+            // global vector (other parts) and y_u (L) / the caller's x (U')
+            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
                 const uint32_t rs = vring_s + uint32_t((h.seq0 + q) & a.ring_mask) * 8u;
 #pragma unroll
                 for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
-            };
-            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
                 double pub[BS];
 #pragma unroll
                 for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
@@ -450,7 +442,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                     for (int r = 0; r < BS; ++r) yu[r] = acc[r];
                 }
             };
-            double acc[BS], acc2[BS];
+            double acc[BS];
             // staged slots: all SR with two groups; with three the registers
             // go to the third group and the blocks are read at the products
             constexpr int SV = G == 2 ? SR : 0;
@@ -461,7 +453,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             };
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
             uint32_t xs[SR];   // its component stride in bytes
-            int idx = 0, idx2 = 0;   // L: the row's U' position; U': its natural row
+            int idx = 0;   // L: the row's U' position; U': its natural row
             if (live) {
                 idx = iarr[gt];
                 init_acc(gt, acc);
@@ -474,10 +466,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                     for (int e = 0; e < BS2; ++e)
                         if (u < SV) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
                 }
-            }
-            if (live2) {
-                idx2 = iarr[q2];
-                init_acc(q2, acc2);
             }
             if (dbg) dbg[1] = clock64();
 #if PS_GPOLL
@@ -548,26 +536,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                 for (int r = 0; r < BS; ++r) acc[r] -= pr[0][r];
                 smem_slots(gt, SR, acc);
                 if (dbg) dbg[4] = clock64();
-                publish_ring(gt, acc);
-                if (!PS_EARLY_HANDOVER) publish(gt, idx, acc);
+                publish(gt, idx, acc);
                 if (dbg) dbg[5] = clock64();
             }
-            if (nr > n1) {
-                // the record's second level: its dependencies on the first level
-                // are in the ring once the group has passed this barrier
-                named_bar_sync(1 + G + grp, PS_NG);
-                if (live2) {
-                    smem_slots(q2, 0, acc2);
-                    publish_ring(q2, acc2);
-                    if (!PS_EARLY_HANDOVER) publish(q2, idx2, acc2);
-                }
-            }
-            // hand record i+1 to the other group, then the global stores (off
-            // the chain), then release record i's ring space (an L record's y_u
-            // stores are read later by the async proxy)
+            // hand record i+1 to the next group, release record i's ring space
+            // (an L record's y_u stores are read later by the async proxy)
             if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % G, 2 * PS_NG);
-            if (PS_EARLY_HANDOVER && live) publish(gt, idx, acc);
-            if (PS_EARLY_HANDOVER && live2) publish(q2, idx2, acc2);
             if (!up) fence_proxy_async_global();
             if (dbg) dbg[6] = clock64();
             mbar_arrive(empty_bar + s);

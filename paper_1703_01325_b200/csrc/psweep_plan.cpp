@@ -312,14 +312,9 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     const int32_t mask = ps.ring - 1;
     std::vector<int32_t> gl;     // a record's deduplicated dependency positions
     std::vector<int32_t> nfar;   // per row of a level group: dependencies outside the ring
-    // records pair two consecutive whole levels when both fit (a level step
-    // inside a record is a group barrier, not a pipeline stage); BILUK_PAIR=1 enables
-    bool pair_levels = false;   // measured neutral at 128^3 (few level pairs fit the record cap)
-    if (const char *env = std::getenv("BILUK_PAIR")) pair_levels = std::atoi(env) != 0;
     struct Chunk {
         size_t a, e;           // rows ord[a, e) of one level
         int64_t lend;          // ring sequence number just past the level
-        bool whole;            // the chunk is its whole level
         int S;
         int64_t far;           // dependencies outside the ring (upper bound, not deduplicated)
     };
@@ -370,28 +365,18 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
                         far = far2;
                         ++e;
                     }
-                    chunks.push_back({a, e, lend, a == g0 && e == ge, S, far});
+                    chunks.push_back({a, e, lend, S, far});
                     a = e;
                 }
                 g0 = ge;
             }
-            // ---- records: one chunk, or two whole consecutive levels
+            // ---- records: one chunk each (pairing two whole levels per record
+            // was measured neutral to slower)
             for (size_t ci0 = 0; ci0 < chunks.size();) {
-                size_t ncs = 1;
-                if (pair_levels && ci0 + 1 < chunks.size()) {
-                    const Chunk &c1 = chunks[ci0], &c2 = chunks[ci0 + 1];
-                    const int nr = int(c2.e - c1.a);
-                    const int S2 = std::max(c1.S, c2.S);
-                    if (c1.whole && c2.whole && c1.e - c1.a <= 255 && c2.e - c2.a <= size_t(ps.nthreads) &&
-                        c1.far + c2.far <= ps.glob_cap && rec_foot_bytes(bs2, vs, nr, S2, int(c1.far + c2.far), up) <= ps.rec_cap)
-                        ncs = 2;
-                }
-                const size_t a = chunks[ci0].a, e = chunks[ci0 + ncs - 1].e;
+                const size_t a = chunks[ci0].a, e = chunks[ci0].e;
                 const int nr = int(e - a);
-                const int n1 = int(chunks[ci0].e - a);
-                int S = 0;
-                for (size_t k2 = 0; k2 < ncs; ++k2) S = std::max(S, chunks[ci0 + k2].S);
-                auto lend_of = [&](size_t q) { return q < chunks[ci0].e ? chunks[ci0].lend : chunks[ci0 + ncs - 1].lend; };
+                const int S = chunks[ci0].S;
+                auto lend_of = [&](size_t) { return chunks[ci0].lend; };
                 gl.clear();
                 for (size_t q = a; q < e; ++q) {
                     const int32_t i = ord[q];
@@ -426,7 +411,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
                 h.nrows = nr;
                 h.S = S;
                 h.nglob = nglob;
-                h.flags = (up ? 1 : 0) | (n1 << 1) | (lvl << 10);
+                h.flags = (up ? 1 : 0) | (nr << 1) | (lvl << 10);
                 h.seq0 = int32_t(seq_base + int32_t(a));
                 h.pos0 = int32_t(b0 + int32_t(a));
                 h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
@@ -461,7 +446,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
                     }
                 }
                 ps.rec.push_back(info);
-                ci0 += ncs;
+                ++ci0;
             }
             if (!up) ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
         }
