@@ -357,8 +357,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             const bool live = gt < nr;
             const int32_t *iarr = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr));
             const int32_t *desc = iarr + nr;
-            const double *vbase = reinterpret_cast<const double *>(rec + h.vals_off) + (up ? size_t(BS2) * nr : 0);
-            const double *vals = vbase + gt;
+            // block values as 32-bit shared byte offsets: element k of row q of
+            // the record's blocks at vb_s + (k * nr + q) * 8 (k = slot * BS2 + e;
+            // a U' record's D^-1 blocks precede them)
+            const uint32_t vstr = uint32_t(nr) * 8u;
+            const uint32_t vb_s = uint32_t(rec + h.vals_off - smem) + (up ? uint32_t(BS2) * vstr : 0u);
+            const uint32_t vals_s = vb_s + uint32_t(gt) * 8u;
             const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off);
             const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
 #if PS_GPOLL
@@ -374,12 +378,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             auto init_acc = [&](int q, double (&acc)[BS]) {
                 const double *inp = inp0 + size_t(q) * VS;
                 if (up) {
-                    const double *dv = vbase - size_t(BS2) * nr + q;
+                    const uint32_t dv_s = vb_s - uint32_t(BS2) * vstr + uint32_t(q) * 8u;
 #pragma unroll
                     for (int r = 0; r < BS; ++r) {
-                        double z = dv[size_t(r) * nr] * inp[0];
+                        double z = lds(dv_s + uint32_t(r) * vstr) * inp[0];
 #pragma unroll
-                        for (int c = 1; c < BS; ++c) z = fma(dv[size_t(c * BS + r) * nr], inp[c], z);
+                        for (int c = 1; c < BS; ++c) z = fma(lds(dv_s + uint32_t(c * BS + r) * vstr), inp[c], z);
                         acc[r] = z;
                     }
                 } else {
@@ -405,15 +409,15 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                     double p2[4][BS];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const double *vv = vbase + q + size_t(sl0 + u) * BS2 * nr;
+                        const uint32_t vv_s = vb_s + uint32_t(q) * 8u + uint32_t((sl0 + u) * BS2) * vstr;
                         const bool on = sl0 + u < S;
 #pragma unroll
-                        for (int r = 0; r < BS; ++r) p2[u][r] = on ? vv[size_t(r) * nr] * xv[u][0] : 0.0;
+                        for (int r = 0; r < BS; ++r) p2[u][r] = on ? lds(vv_s + uint32_t(r) * vstr) * xv[u][0] : 0.0;
 #pragma unroll
                         for (int c = 1; c < BS; ++c)
 #pragma unroll
                             for (int r = 0; r < BS; ++r)
-                                if (on) p2[u][r] = fma(vv[size_t(c * BS + r) * nr], xv[u][c], p2[u][r]);
+                                if (on) p2[u][r] = fma(lds(vv_s + uint32_t(c * BS + r) * vstr), xv[u][c], p2[u][r]);
                     }
 #pragma unroll
                     for (int r = 0; r < BS; ++r) acc[r] -= (p2[0][r] + p2[1][r]) + (p2[2][r] + p2[3][r]);
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             double v[SV > 0 ? SV : 1][BS2] = {};
             // element e of slot u's block of this thread's row (registers, or shared memory)
             auto vblk = [&](int u, int e) -> double {
-                return u < SV ? v[u][e] : (u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0);
+                return u < SV ? v[u][e] : (u < S ? lds(vals_s + uint32_t(u * BS2 + e) * vstr) : 0.0);
             };
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
             uint32_t xs[SR];   // its component stride in bytes
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                     xs[u] = d >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
 #pragma unroll
                     for (int e = 0; e < BS2; ++e)
-                        if (u < SV) v[u][e] = u < S ? vals[size_t(u * BS2 + e) * nr] : 0.0;
+                        if (u < SV) v[u][e] = u < S ? lds(vals_s + uint32_t(u * BS2 + e) * vstr) : 0.0;
                 }
             }
             if (dbg) dbg[1] = clock64();
