@@ -244,11 +244,20 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     const int bs = p.bs, bs2 = bs * bs, vs = ps_vec_stride(bs);
     const int64_t n = p.n;
     // ---- choose the partition ---------------------------------------------------
-    // structured grids: (y, z) columns; anything else: contiguous row ranges.
+    // ILU(0) on a structured grid: (y, z) columns.  With fill (k >= 1) a row
+    // also depends on rows of the next column over in y (fill entries such as
+    // (x+1, y-1)), so column parts wait on each other level after level;
+    // contiguous row ranges keep every dependency flowing from a part to
+    // later parts and measured 1.5x faster.  Anything that is
+    // not a grid: contiguous.  BILUK_PARTITION=columns|contiguous overrides.
     // P: every SM for large systems, else the cost model's choice.
     int64_t g[3] = {0, 0, 0};
-    bool grid = detect_grid(p, g);
-    if (const char *env = std::getenv("BILUK_PARTITION")) grid = grid && std::string(env) != "contiguous";
+    const bool is_grid = detect_grid(p, g);
+    bool grid = is_grid && p.k == 0;
+    if (const char *env = std::getenv("BILUK_PARTITION")) {
+        if (std::string(env) == "contiguous") grid = false;
+        if (std::string(env) == "columns") grid = is_grid;
+    }
     int P = parts;
     if (const char *env = std::getenv("BILUK_PARTS")) P = std::atoi(env);
     Partition pt;
