@@ -7,15 +7,16 @@ mapping.  Every numeric step of the path runs as hand-written sm_100a CUDA in
 device buffers only.  There is no CPU fallback.
 """
 
-from .errors import FactorizationError, SingularBlockError, StructuralError
+from .errors import FactorizationError, MatrixMarketError, SingularBlockError, StructuralError
 from .factor import BlockIlukFactors, build_preconditioner, symbolic_phase
 from .krylov import SolverConfig, SolveStats, bicgstab, bicgstab_batched, gmres
-from .sparse import (BcsrMatrix, CsrMatrix, PatternMatrix, bcsr_from_csr, block_diagonal, csr_expand,
-                     csr_from_triplets, extract_point_pattern)
+from .sparse import (BcsrMatrix, CsrMatrix, PatternMatrix, assemble_csr, bcsr_from_csr, block_diagonal,
+                     csr_expand, csr_from_triplets, extract_point_pattern)
+from .matrix_market import read_matrix_market
 from .trisolve import (LevelSchedule, TriangularOperand, apply_preconditioner, apply_preconditioner_many,
                        build_level_schedule, strict_triangle)
 from .device import DeviceOperator
-from .synthetic import reservoir_block_grid
+from .synthetic import gen_poisson_3d, reservoir_block_grid
 
 __version__ = "0.1.0"
 
@@ -33,8 +34,9 @@ def spmv(a, x, workers=1):
 
 __all__ = [
     "BcsrMatrix", "BlockIlukFactors", "CsrMatrix", "DeviceOperator", "FactorizationError", "LevelSchedule",
-    "PatternMatrix", "SingularBlockError", "SolveStats", "SolverConfig", "StructuralError", "TriangularOperand",
-    "apply_preconditioner", "apply_preconditioner_many", "bcsr_from_csr", "bicgstab", "bicgstab_batched", "block_diagonal", "build_level_schedule", "build_preconditioner",
-    "csr_expand", "csr_from_triplets", "extract_point_pattern", "gmres", "reservoir_block_grid", "spmv",
-    "strict_triangle", "symbolic_phase", "__version__",
+    "MatrixMarketError", "PatternMatrix", "SingularBlockError", "SolveStats", "SolverConfig", "StructuralError",
+    "TriangularOperand", "apply_preconditioner", "apply_preconditioner_many", "assemble_csr", "bcsr_from_csr",
+    "bicgstab", "bicgstab_batched", "block_diagonal", "build_level_schedule", "build_preconditioner",
+    "csr_expand", "csr_from_triplets", "extract_point_pattern", "gen_poisson_3d", "gmres", "read_matrix_market",
+    "reservoir_block_grid", "spmv", "strict_triangle", "symbolic_phase", "__version__",
 ]

@@ -19,3 +19,15 @@ class FactorizationError(RuntimeError):
 
 class SingularBlockError(FactorizationError):
     """A diagonal block was singular to working precision."""
+
+
+class MatrixMarketError(ValueError):
+    """A Matrix Market file could not be parsed (reference errors.py MatrixMarketError).
+
+    ``line`` holds the 1-based physical line number of the problem; the
+    message starts with ``"line <n>: "`` when it is known.
+    """
+
+    def __init__(self, message, line=None):
+        self.line = line
+        super().__init__(message if line is None else f"line {line}: {message}")

@@ -15,7 +15,7 @@ import numpy as np
 from .errors import StructuralError
 
 __all__ = ["CsrMatrix", "BcsrMatrix", "PatternMatrix", "bcsr_from_csr", "csr_expand",
-           "extract_point_pattern", "csr_from_triplets", "as_bsr", "block_diagonal"]
+           "extract_point_pattern", "csr_from_triplets", "assemble_csr", "as_bsr", "block_diagonal"]
 
 
 def _index_array(a, name):
@@ -181,6 +181,27 @@ class PatternMatrix:
 
     def __repr__(self):
         return f"PatternMatrix(n={self.n}, nnz={self.nnz})"
+
+
+def assemble_csr(num_rows, num_cols, rows, cols, vals):
+    """CSR from parallel (row, col, value) arrays, duplicates summed (reference sparse.py:224-245)."""
+    r = np.asarray(rows, dtype=np.int64).ravel()
+    c = np.asarray(cols, dtype=np.int64).ravel()
+    v = np.asarray(vals, dtype=np.float64).ravel()
+    if not (r.size == c.size == v.size):
+        raise StructuralError("triplet arrays must have equal length")
+    if r.size == 0:
+        return CsrMatrix(num_rows, num_cols, np.zeros(num_rows + 1, np.int64), [], [])
+    if r.min() < 0 or r.max() >= num_rows or c.min() < 0 or c.max() >= num_cols:
+        raise StructuralError("triplet index outside the matrix")
+    key = r * num_cols + c
+    order = np.argsort(key, kind="stable")
+    key, v = key[order], v[order]
+    uniq, first = np.unique(key, return_index=True)
+    summed = np.add.reduceat(v, first)
+    rp = np.zeros(num_rows + 1, np.int64)
+    np.cumsum(np.bincount(uniq // num_cols, minlength=num_rows), out=rp[1:])
+    return CsrMatrix(num_rows, num_cols, rp, uniq % num_cols, summed)
 
 
 def csr_from_triplets(num_rows, num_cols, entries):

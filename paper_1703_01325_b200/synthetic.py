@@ -48,6 +48,21 @@ def poisson7_pattern(nx: int, ny: int, nz: int):
     return rp, ci
 
 
+def gen_poisson_3d(nx: int, ny: int, nz: int):
+    """The reference's 7-point operator as a CsrMatrix (reference poisson.py:11-52).
+
+    6 on the diagonal, -1 for each existing axis neighbour (Dirichlet
+    truncation), x-fastest numbering, columns increasing within a row.
+    """
+    from .errors import StructuralError
+    from .sparse import CsrMatrix
+    if min(int(nx), int(ny), int(nz)) < 1:
+        raise StructuralError("grid dimensions must be at least 1")
+    rp, ci = poisson7_pattern(nx, ny, nz)
+    rows = np.repeat(np.arange(rp.size - 1, dtype=np.int64), np.diff(rp))
+    return CsrMatrix(rp.size - 1, rp.size - 1, rp, ci, np.where(ci == rows, 6.0, -1.0))
+
+
 def reservoir_block_grid(nx: int, ny: int, nz: int, bs: int, seed: int = 0,
                          sigma: float = 1.0, eps: float = 0.2, acc: float = 1e-2):
     """Return (n, bs, row_ptr, col_idx, values) of the synthetic block matrix."""
