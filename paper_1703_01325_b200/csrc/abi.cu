@@ -140,7 +140,9 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     // BILUK_ENGINE overrides.
     Plan &P = h->p;
     const char *env = std::getenv("BILUK_ENGINE");
-    P.engine = bs <= 4 ? 1 : 0;
+    // (ILU(2) and beyond on large systems plan far over the records-per-part
+    // limit -- 128^3: 1352 -- so they skip the partitioned planning outright)
+    P.engine = (bs <= 4 && !(k >= 2 && n > (int64_t(3) << 19))) ? 1 : 0;
     if (env) P.engine = std::atoi(env) == 0 ? 0 : 1;
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
