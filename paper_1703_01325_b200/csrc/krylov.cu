@@ -363,7 +363,7 @@ int biluk_bicgstab(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *us
                    int64_t hist_cap, void *stream) {
     if (!A || !A->o.valued) return fail(BILUK_EARG, "operator has no values");
     if (A->o.n != A->o.ncols) return fail(BILUK_EARG, "bicgstab requires a square matrix");
-    if (M && (!M->p.factored || M->p.n != A->o.n || M->p.bs != A->o.bs))
+    if (M && (!M->p.factored || M->p.n * M->p.bs != A->o.n * A->o.bs))   // vectors must match; blockings may differ
         return fail(BILUK_EARG, "preconditioner does not match the operator");
     if (max_iters < 1 || !(rel_tol > 0.0)) return fail(BILUK_EARG, "bad solver configuration");
     const int64_t len = A->o.n * A->o.bs;
@@ -523,7 +523,7 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
                            double rel_tol, double *stats, void *stream) {
     if (!A || !A->o.valued) return fail(BILUK_EARG, "operator has no values");
     if (A->o.n != A->o.ncols) return fail(BILUK_EARG, "bicgstab requires a square matrix");
-    if (M && (!M->p.factored || M->p.n != A->o.n || M->p.bs != A->o.bs))
+    if (M && (!M->p.factored || M->p.n * M->p.bs != A->o.n * A->o.bs))   // vectors must match; blockings may differ
         return fail(BILUK_EARG, "preconditioner does not match the operator");
     if (max_iters < 1 || !(rel_tol > 0.0)) return fail(BILUK_EARG, "bad solver configuration");
     if (nsys < 1 || !seg || !stats) return fail(BILUK_EARG, "bad batch description");
@@ -652,7 +652,7 @@ int biluk_gmres(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user,
                 double *stats, double *history, int64_t hist_cap, void *stream) {
     if (!A || !A->o.valued) return fail(BILUK_EARG, "operator has no values");
     if (A->o.n != A->o.ncols) return fail(BILUK_EARG, "gmres requires a square matrix");
-    if (M && (!M->p.factored || M->p.n != A->o.n || M->p.bs != A->o.bs))
+    if (M && (!M->p.factored || M->p.n * M->p.bs != A->o.n * A->o.bs))   // vectors must match; blockings may differ
         return fail(BILUK_EARG, "preconditioner does not match the operator");
     if (restart < 1 || max_iters < 1 || !(rel_tol > 0.0) || !(abs_tol > 0.0))
         return fail(BILUK_EARG, "bad solver configuration");

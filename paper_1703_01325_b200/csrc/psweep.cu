@@ -2,24 +2,30 @@
 //   L y = b,  z = D^-1 y,  U' x = z      (apply_preconditioner, trisolve.py:121-182)
 // and the device pack of its records from the factors.
 //
-// One CTA per part (a contiguous block-row range, psweep_plan.cpp), all CTAs
-// co-resident (cooperative launch).  Inside a CTA:
-//   * warp NW (the last one) is the PRODUCER + PREFETCHER: lane 0 streams the
-//     part's records into a shared-memory ring with cp.async.bulk (1-D TMA,
-//     evict-first), and the warp fetches every value a record needs from
-//     global memory -- the rows' own inputs (b for L, y for U') and every
-//     dependency that is not in the on-chip ring (other parts, or rows of this
-//     part that left the ring) -- polling the parity tags, into a second ring;
-//   * warps 0..NW-1 COMPUTE, one thread per block row of the record:
+// One CTA per part (grid columns for ILU(0), contiguous row ranges with fill;
+// psweep_plan.cpp), all CTAs co-resident (cooperative launch).  A part's rows
+// are cut into RECORDS (<= 128 rows of one level, L records then U' records).
+// Inside a CTA:
+//   * G COMPUTE GROUPS of 128 threads (G = 3 for ILU(0), 2 with fill) take
+//     records round-robin, one thread per block row:
 //       L :  y_i = b_i - sum_j L_ij y_j
 //       U':  x_i = D_i^-1 y_i - sum_j U'_ij x_j
-//     reading dependencies from shared memory only (the vector ring of this
-//     part's recent results, or the fetched values), then publish the row to
-//     the ring, to the parity-tagged global vector (other parts poll it) and,
-//     for U', to the caller's x.  A named barrier ends every record.
-// L dependencies live in this or EARLIER parts, U' dependencies in this or
-// LATER parts (and y_i in this part): part 0's L and part P-1's U' never wait
-// on another part, so by induction every CTA finishes (no deadlock).
+//     Off the chain, a group stages its next record (indices, b or D^-1 y,
+//     the shared addresses of every dependency) and fetches the record's
+//     dependencies held by other parts from the parity-tagged global vector
+//     (tag-polled; the first load overlaps the staging).  On the chain -- a
+//     named-barrier hand-over from the previous record's group -- it loads
+//     the dependencies from shared memory (the part's vector ring or the
+//     fetched values), forms the products and publishes the row to the ring,
+//     to the tagged global vector (other parts poll it) and to y_u (L, the
+//     U' input) or the caller's x (U').
+//   * two PRODUCER warps (even / odd records, each in its half of the data
+//     ring) stream records and their rows' inputs (b_perm / y_u, position
+//     ordered) into shared memory with cp.async.bulk on mbarriers, pulling
+//     records ahead into L2 with cp.async.bulk.prefetch.L2.
+// Every CTA walks its rows in global level order, L then U', and every
+// dependency has a lower level, so the CTA holding the lowest unfinished row
+// is never blocked -- for any row-to-part assignment (no deadlock).
 #include <cstdint>
 
 #include "biluk_internal.h"
@@ -34,11 +40,7 @@ namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
 // compute groups (round-robin over records) are a template parameter G: 2 or 3
-#ifndef PS_GPOLL
-#define PS_GPOLL 1                    // 1: each compute group fetches its records' dependencies itself
-#endif
-constexpr int PS_NPOLL = PS_GPOLL ? 0 : 2;   // poll warps (alternate records)
-constexpr int PS_NAUX = 2 + PS_NPOLL; // two producers (even / odd records) + poll warps
+constexpr int PS_NAUX = 2;            // two producer warps (even / odd records) after the compute groups
 constexpr int PS_PF = 16;             // records prefetched into L2 ahead of their bulk copy
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -137,15 +139,12 @@ __device__ __forceinline__ bool mbar_wait_or_abort(uint64_t *bar, uint32_t phase
 
 template <int BS, int G>
 __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(const PSweepArgs a) {
-    constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the producers (and poll warps)
+    constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the two producers
     constexpr int BS2 = BS * BS;
     constexpr int VS = ps_vec_stride(BS);
     constexpr int K = PS_KSLOTS;
-    constexpr int EPL = ps_glob_cap(BS) / 32;   // dependency entries per poll lane
-    static_assert(PS_NPOLL == 0 || K % PS_NPOLL == 0, "poll warps must own whole ring slots");
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[K];    // record bytes + inputs landed (two bulk copies)
-    __shared__ __align__(8) uint64_t dep_bar[K];     // dependencies fetched (poll warp)
     __shared__ __align__(8) uint64_t empty_bar[K];   // record consumed (every thread of a compute group)
     __shared__ uint32_t slot_off[K];
     __shared__ int abort_flag;   // a wait timed out somewhere (the device status is sticky)
@@ -161,7 +160,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
     if (tid == 0) {
         for (int s = 0; s < K; ++s) {
             mbar_init(full_bar + s, 1);
-            mbar_init(dep_bar + s, 1);
             mbar_init(empty_bar + s, PS_NG);
         }
         abort_flag = 0;
@@ -268,64 +266,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
         }
         // never leave the CTA with copies in flight into its shared memory
         for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + (pp + 2 * g) % K, uint32_t((pp + 2 * g) / K) & 1u);
-#if !PS_GPOLL
-    } else if (warp > PS_NW + 1) {
-        // ============ poll: dependencies outside the on-chip ring ==============
-        // warp p owns records p, p + NPOLL, ...; all its loads of a round are
-        // in flight before any tag is checked (one L2 round trip per round)
-        const int pw = warp - PS_NW - 2;
-        for (int i = pw; i < nrec; i += PS_NPOLL) {
-            const int s = i % K;
-            if (!mbar_wait_or_abort(full_bar + s, uint32_t(i / K) & 1u, &abort_flag, a)) break;
-            if (a.trace && lane == 0) a.trace[size_t(r0 + i) * 8 + 1] = globaltimer();
-            unsigned char *rec = dring + slot_off[s];
-            const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
-            const int nr = h.nrows, ng = h.nglob;
-            const int32_t *gpos = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr)) + nr + h.S * nr;
-            double *dst = reinterpret_cast<double *>(rec + h.in_off) + size_t(nr) * VS;   // deps, component-major
-            const double *vec = (h.flags & 1) ? a.x_t : a.y_t;
-            uint32_t pend = 0;
-            int32_t pos[EPL];
-#pragma unroll
-            for (int m = 0; m < EPL; ++m) {
-                const int e = lane + 32 * m;
-                pos[m] = e < ng ? gpos[e] : 0;
-                if (e < ng) pend |= 1u << m;
-            }
-            uint64_t t0 = 0;
-            uint32_t spins = 0;
-            bool dead = false;
-            while (__any_sync(0xffffffffu, pend)) {
-                double v[EPL][BS];
-#pragma unroll
-                for (int m = 0; m < EPL; ++m)
-                    if (pend & (1u << m)) ld_row<BS>(vec + size_t(pos[m]) * VS, v[m]);
-#pragma unroll
-                for (int m = 0; m < EPL; ++m)
-                    if (pend & (1u << m)) {
-                        uint32_t ok = 1;
-#pragma unroll
-                        for (int q = 0; q < BS; ++q) ok &= (tag_of(v[m][q]) == par);
-                        if (ok) {
-#pragma unroll
-                            for (int q = 0; q < BS; ++q) dst[size_t(q) * ng + lane + 32 * m] = untag(v[m][q]);
-                            pend &= ~(1u << m);
-                        }
-                    }
-                if (pend && ps_timed_out(t0, spins, a)) {
-                    abort_flag = 1;
-                    dead = true;
-                }
-                if (__any_sync(0xffffffffu, dead)) break;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                if (a.trace) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
-                mbar_arrive(dep_bar + s);
-            }
-            if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
-        }
-#endif
     } else {
         // ========================= compute warps ==============================
         // two groups of PS_NG threads take alternate records (ping-pong).  A
@@ -365,7 +305,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             const uint32_t vals_s = vb_s + uint32_t(gt) * 8u;
             const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off);
             const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
-#if PS_GPOLL
             // dependencies outside the ring: thread e fetches entry e (tag-polled);
             // the first load is issued here so its round trip overlaps the prep
             const int32_t *gpos = desc + size_t(S) * nr;
@@ -373,7 +312,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             const bool dneed = gt < ng;
             double dval[BS];
             if (dneed) ld_row<BS>(gvec + size_t(gpos[gt]) * VS, dval);
-#endif
             // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
             auto init_acc = [&](int q, double (&acc)[BS]) {
                 const double *inp = inp0 + size_t(q) * VS;
@@ -472,7 +410,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                 }
             }
             if (dbg) dbg[1] = clock64();
-#if PS_GPOLL
             {
                 auto fetch_dep = [&](int e, double (&dv)[BS], bool loaded) {
                     const double *src = gvec + size_t(gpos[e]) * VS;
@@ -501,17 +438,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                 if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
                 if (i == 0) named_bar_sync(1 + G + grp, PS_NG);   // the fetched values, to the whole group
             }
-#else
-            if (!mbar_wait_or_abort(dep_bar + s, ph, &abort_flag, a)) break;
-#endif
             if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 4] = globaltimer();
             if (dbg) dbg[2] = clock64();
             // the other group has published record i-1
             if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
             if (dbg) dbg[3] = clock64();
-#if PS_GPOLL
             if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
-#endif
             if (live) {
                 // register-staged slots: every dependency load first, then the
                 // products, summed as a tree and subtracted once
