@@ -361,8 +361,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
                     for (int r = 0; r < BS; ++r) acc[r] -= (p2[0][r] + p2[1][r]) + (p2[2][r] + p2[3][r]);
                 }
             };
-            // publish row q: ring (this part), tagged global vector (other parts),
-            // and y for this part's U' sweep (L) / the caller's x (U')
             // publish row q: the ring (this part's next levels), the tagged
             // global vector (other parts) and y_u (L) / the caller's x (U')
             auto publish = [&](int q, int idx, const double (&acc)[BS]) {
@@ -396,7 +394,20 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
             uint32_t xs[SR];   // its component stride in bytes
             int idx = 0;   // L: the row's U' position; U': its natural row
-            if (live) {
+            // rows longer than the staged slots in a record of few rows: TPR
+            // threads per row share its slots (strided) and sum by shuffles,
+            // so the idle threads of a short record shorten the chain
+            const int tpr = S > SR ? (nr <= 16 ? 8 : nr <= 32 ? 4 : nr <= 64 ? 2 : 1) : 1;
+            const int tq = gt / tpr, tj = gt & (tpr - 1);   // split: row and slot lane
+            const bool tlive = tq < nr;
+            if (tpr > 1) {
+#pragma unroll
+                for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+                if (tlive && tj == 0) {
+                    idx = iarr[tq];
+                    init_acc(tq, acc);
+                }
+            } else if (live) {
                 idx = iarr[gt];
                 init_acc(gt, acc);
 #pragma unroll
@@ -444,7 +455,34 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
             if (dbg) dbg[3] = clock64();
             if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
-            if (live) {
+            if (tpr > 1) {
+                if (tlive) {
+                    for (int u = tj; u < S; u += tpr) {
+                        const int32_t d = desc[u * nr + tq];
+                        const uint32_t ad = d >= 0 ? vring_s + uint32_t(d) * 8u : dep_s + uint32_t(-d - 1) * 8u;
+                        const uint32_t st = d >= 0 ? uint32_t(RS) * 8u : uint32_t(ng) * 8u;
+                        double x[BS];
+#pragma unroll
+                        for (int c = 0; c < BS; ++c) x[c] = lds(ad + uint32_t(c) * st);
+                        const uint32_t vv_s = vb_s + uint32_t(tq) * 8u + uint32_t(u * BS2) * vstr;
+                        double pu[BS];
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) pu[r] = lds(vv_s + uint32_t(r) * vstr) * x[0];
+#pragma unroll
+                        for (int c = 1; c < BS; ++c)
+#pragma unroll
+                            for (int r = 0; r < BS; ++r) pu[r] = fma(lds(vv_s + uint32_t(c * BS + r) * vstr), x[c], pu[r]);
+#pragma unroll
+                        for (int r = 0; r < BS; ++r) acc[r] -= pu[r];
+                    }
+                }
+                for (int o = tpr >> 1; o > 0; o >>= 1)
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+                if (dbg) dbg[4] = clock64();
+                if (tlive && tj == 0) publish(tq, idx, acc);
+                if (dbg) dbg[5] = clock64();
+            } else if (live) {
                 // register-staged slots: every dependency load first, then the
                 // products, summed as a tree and subtracted once
                 double x[SR][BS];
