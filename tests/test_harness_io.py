@@ -107,3 +107,16 @@ def test_sweep_on_gpu_matches_oracle_iterations(cuda_ok, capsys):
         _, its, conv, _, _ = orc.gmres(mv, b, precond=f.apply, restart=30)
         assert conv and abs(its - r.iterations) <= 1
     assert harness.main(["--poisson", "4", "4", "4", "--block-sizes", "1,2", "--format", "csv"]) == 0
+
+
+@pytest.mark.parametrize("fmt", ["csv", "table"])
+def test_reports_match_reference_golden(fmt):
+    """Byte-identical to the reference's emit_report (tests/golden/make_harness_golden.py)."""
+    import os
+    recs = [harness.BenchRecord(1, 0, 1, 0.5, 0.25, 10, True, 1e-7),
+            harness.BenchRecord(1, 0, 4, 0.5, 0.125, 10, True, 1e-7),
+            harness.BenchRecord(2, 1, 1, 0.1, 0.3, 3, False, 2e-3),
+            harness.BenchRecord(4, 2, 1, 1.0 / 3.0, 0.0, 0, True, 0.0)]
+    path = os.path.join(os.path.dirname(__file__), "golden", f"harness_report_{fmt}.txt")
+    with open(path) as fh:
+        assert harness.emit_report(recs, fmt) == fh.read()
