@@ -135,22 +135,21 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     // §3): the partitioned sweep wins while its records per part stay few --
     // always for ILU(0) with b <= 3 (grid columns); ILU(0) with b = 4 up to
     // ~400 records per part (100^3 yes, 128^3 no); with fill (contiguous
-    // parts) up to ~1000 (128^3 ILU(1) yes, 128^3 ILU(2) no).  Larger blocks
-    // and batches of many systems go to the tiled level-order sweep.
+    // parts) up to ~1500 (128^3 ILU(2): 1352, yes).  Larger blocks and
+    // batches of many systems go to the tiled level-order sweep.
     // BILUK_ENGINE overrides.
     Plan &P = h->p;
     const char *env = std::getenv("BILUK_ENGINE");
-    // (ILU(2) and beyond on large systems plan far over the records-per-part
-    // limit -- 128^3: 1352 -- so they skip the partitioned planning outright)
-    P.engine = (bs <= 4 && !(k >= 2 && n > (int64_t(3) << 19))) ? 1 : 0;
+    P.engine = bs <= 4 ? 1 : 0;
     if (env) P.engine = std::atoi(env) == 0 ? 0 : 1;
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
         const double per_part = P.ps.P > 0 ? double(P.ps.rec.size()) / P.ps.P : 0.0;
-        const double limit = k >= 1 ? 1000.0 : (bs <= 3 ? 1e30 : 400.0);
+        const double limit = k >= 1 ? 1500.0 : (bs <= 3 ? 1e30 : 400.0);
         // three compute groups (blocks read at the products) measured faster
-        // for ILU(0); two (blocks staged in registers) for ILU(1)
-        P.ps.groups = k == 0 ? 3 : 2;
+        // than two (blocks staged in registers) for every case; BILUK_GROUPS=2
+        // selects the two-group kernel
+        P.ps.groups = 3;
         if (const char *g = std::getenv("BILUK_GROUPS")) P.ps.groups = std::atoi(g) == 3 ? 3 : 2;
         if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;
