@@ -140,7 +140,10 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     // BILUK_ENGINE overrides.
     Plan &P = h->p;
     const char *env = std::getenv("BILUK_ENGINE");
-    P.engine = bs <= 4 ? 1 : 0;
+    // (very large operators -- e.g. the 64-system batch, 16.8 M block rows --
+    // plan far over the records-per-part limit; they skip the partitioned
+    // planning, which would only be discarded, outright)
+    P.engine = (bs <= 4 && n <= (int64_t(1) << 22)) ? 1 : 0;
     if (env) P.engine = std::atoi(env) == 0 ? 0 : 1;
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
