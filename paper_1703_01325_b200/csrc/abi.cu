@@ -164,6 +164,13 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     }
     if (P.engine == 0) {
         rc = plan_tiles(P);
+        // a tile stages all its rows padded to its longest row: one stage must
+        // fit in shared memory (very long rows -- e.g. an arrowhead -- do not)
+        const int64_t stage = std::max<int64_t>(128, std::max(P.sl.max_rec, P.su.max_rec));
+        if (rc == BILUK_OK && stage + 16 > int64_t(smem) - 4096)
+            rc = fail(BILUK_EUNSUPPORTED, "a factor row has " + std::to_string(std::max(P.sl.max_slots, P.su.max_slots)) +
+                                              " off-diagonal blocks: its sweep tile (" + std::to_string(stage) +
+                                              " bytes) exceeds shared memory");
         if (rc != BILUK_OK) {
             delete h;
             return rc;

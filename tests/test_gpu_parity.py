@@ -311,3 +311,54 @@ def test_apply_many_pipelined_equals_single_applies(b2):
         b2.apply_preconditioner_many(f, rhs[:, :-1])
     with pytest.raises(ValueError):
         b2.apply_preconditioner_many(f, torch.from_numpy(rhs).cuda())
+
+
+def _bsr_from_dense_blocks(b2, nb, bs, blocks):
+    """BcsrMatrix from {(i, j): (bs, bs) block} (column-major inside each block)."""
+    rp, ci, vals = [0], [], []
+    for i in range(nb):
+        for j in sorted(c for (r, c) in blocks if r == i):
+            ci.append(j)
+            vals.extend(np.asarray(blocks[(i, j)], dtype=np.float64).T.reshape(-1))
+        rp.append(len(ci))
+    return b2.BcsrMatrix(bs, nb, nb, np.array(rp), np.array(ci), np.array(vals))
+
+
+@pytest.mark.parametrize("engine", ["0", "1"])
+def test_edge_shapes_match_oracle(b2, monkeypatch, engine):
+    """One block row; a block-diagonal matrix (one level); an arrowhead whose
+    first row and column touch every row (a long row, a long column); a 1x1
+    scalar system."""
+    monkeypatch.setenv("BILUK_ENGINE", engine)
+    rng = np.random.default_rng(77)
+    cases = []
+    d = rng.standard_normal((3, 3)) + 4 * np.eye(3)
+    cases.append((_bsr_from_dense_blocks(b2, 1, 3, {(0, 0): d}), [0, 2]))
+    diag = {(i, i): rng.standard_normal((2, 2)) + 3 * np.eye(2) for i in range(50)}
+    cases.append((_bsr_from_dense_blocks(b2, 50, 2, diag), [0, 1]))
+    arrow = {(i, i): rng.standard_normal((3, 3)) + 40 * np.eye(3) for i in range(60)}
+    for i in range(1, 60):
+        arrow[(0, i)] = 0.1 * rng.standard_normal((3, 3))
+        arrow[(i, 0)] = 0.1 * rng.standard_normal((3, 3))
+    cases.append((_bsr_from_dense_blocks(b2, 60, 3, arrow), [0, 1]))
+    cases.append((b2.csr_from_triplets(1, 1, [(0, 0, 2.5)]), [0, 3]))
+    for a, ks in cases:
+        nb = a.num_block_rows if hasattr(a, "num_block_rows") else a.num_rows
+        bs = a.block_size if hasattr(a, "block_size") else 1
+        for k in ks:
+            f = b2.build_preconditioner(a, k)
+            of = orc.build_preconditioner(nb, bs, a.row_ptr, a.col_idx, a.values, k)
+            rhs = rng.standard_normal(nb * bs)
+            assert rel_err(b2.apply_preconditioner(f, rhs), of.apply(rhs)) <= TOL
+
+
+def test_rows_too_long_for_the_sweep_fail_clearly(b2, monkeypatch):
+    """A row whose sweep tile cannot be staged raises NotImplementedError naming the row length."""
+    monkeypatch.setenv("BILUK_ENGINE", "0")
+    rng = np.random.default_rng(5)
+    arrow = {(i, i): rng.standard_normal((3, 3)) + 40 * np.eye(3) for i in range(400)}
+    for i in range(1, 400):
+        arrow[(0, i)] = 0.1 * rng.standard_normal((3, 3))
+        arrow[(i, 0)] = 0.1 * rng.standard_normal((3, 3))
+    with pytest.raises(NotImplementedError, match="off-diagonal blocks"):
+        b2.build_preconditioner(_bsr_from_dense_blocks(b2, 400, 3, arrow), 0)
