@@ -163,7 +163,7 @@ struct PRecInfo {       // 64 bytes: one per record, read by the producer, the g
 // doubles per position of the partitioned sweep's vectors (>= 2: 16-byte rows)
 BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
 // fetched dependencies per record (a multiple of 32: one per poll lane and round)
-BILUK_HD constexpr inline int ps_glob_cap(int bs) { return bs <= 4 ? 256 : 128; }
+BILUK_HD constexpr inline int ps_glob_cap(int) { return 1024; }   // fetched dependencies per record (the groups loop over them)
 constexpr int PS_KSLOTS = 16;      // records in flight per CTA (mbarrier sets)
 
 // an assignment of block rows to parts (any assignment is deadlock-free:
