@@ -41,7 +41,7 @@ namespace {
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
 // compute groups (round-robin over records) are a template parameter G: 2 or 3
 constexpr int PS_NAUX = 2;            // two producer warps (even / odd records) after the compute groups
-constexpr int PS_PF = 16;             // records prefetched into L2 ahead of their bulk copy
+constexpr int PS_PF = 2;              // records pulled into L2 ahead of their bulk copy (2 measured best of 0-32)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
