@@ -40,7 +40,10 @@ namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
 // compute groups (round-robin over records) are a template parameter G: 2 or 3
-constexpr int PS_NAUX = 2;            // two producer warps (even / odd records) after the compute groups
+#ifndef PS_NPROD
+#define PS_NPROD 2                    // producer warps (record r served by producer r % PS_NPROD)
+#endif
+constexpr int PS_NAUX = PS_NPROD;     // the producer warps come after the compute groups
 constexpr int PS_PF = 2;              // records pulled into L2 ahead of their bulk copy (2 measured best of 0-32)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
     for (int x = tid; x < VS; x += blockDim.x) vring[size_t(x) * RS + a.ring_mask + 1] = 0.0;
     __syncthreads();
 
-    if (warp == PS_NW || warp == PS_NW + 1) {
+    if (warp >= PS_NW && warp < PS_NW + PS_NPROD) {
         // ============ producers: bulk copies into the record ring ==============
         // producer pp serves records pp, pp+2, ... (the records of compute
         // group pp) in its own half of the ring.  Per record two bulk copies on
@@ -179,8 +182,9 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
         // this part's L sweep is complete).  Space is recycled in record order
         // (empty barriers); records are pulled into L2 ahead so the copies are short.
         const int pp = warp - PS_NW;
-        const int nk = (nrec - pp + 1) / 2;   // records of this producer: pp + 2k
-        const uint32_t half = (a.data_bytes / 2) & ~15u;
+        constexpr int NP = PS_NPROD;
+        const int nk = (nrec - pp + NP - 1) / NP;   // records of this producer: pp + NP k
+        const uint32_t half = (a.data_bytes / NP) & ~15u;
         unsigned char *ring = dring + pp * half;
         const uint64_t pol = policy_evict_first();
         uint32_t dhead = 0;
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
         uint32_t cur_bytes = 0, cur_foot = 0, cur_pm = 0, nxt_bytes = 0, nxt_foot = 0, nxt_pm = 0;
         uint32_t cur_nr = 0, nxt_nr = 0;
         auto fetch = [&](int k, uint64_t &off, uint32_t &bytes, uint32_t &foot, uint32_t &pos0u, uint32_t &nr) {
-            const PRecInfo &ri = a.rec[r0 + pp + 2 * k];
+            const PRecInfo &ri = a.rec[r0 + pp + NP * k];
             off = ri.off;
             bytes = ri.bytes;
             foot = ri.foot;
@@ -204,7 +208,8 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
         };
         if (lane < nk) fetch(lane, cur_off, cur_bytes, cur_foot, cur_pm, cur_nr);
         if (32 + lane < nk) fetch(32 + lane, nxt_off, nxt_bytes, nxt_foot, nxt_pm, nxt_nr);
-        for (int j = lane; j < PS_PF / 2 && j < nk; j += 32) bulk_prefetch_l2(a.recs + cur_off, cur_bytes);
+        constexpr int PFO = PS_PF / NP > 0 ? PS_PF / NP : 1;   // own records prefetched ahead
+        for (int j = lane; j < PFO && j < nk; j += 32) bulk_prefetch_l2(a.recs + cur_off, cur_bytes);
         for (; issued < nk; ++issued) {
             if (issued > 0 && (issued & 31) == 0) {   // slide the window by 32 records
                 cur_off = nxt_off;
@@ -223,33 +228,33 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             const uint32_t nr = __shfl_sync(0xffffffffu, cur_nr, jl);
             const bool up = pm >> 31;
             const uint32_t pos0 = pm & 0x7fffffffu;
-            const int rr = pp + 2 * issued;   // record index
+            const int rr = pp + NP * issued;   // record index
             bool ok = true;
             if (up && !up_ready) {
                 // y_u is written by this part's L sweep: every L record of both
                 // groups must be consumed before the first U' input copy
-                for (; ok && oldest < issued; ++oldest) ok = wait_rec(pp + 2 * oldest);
+                for (; ok && oldest < issued; ++oldest) ok = wait_rec(pp + NP * oldest);
                 if (ok && rr >= 1) ok = wait_rec(rr - 1);
                 up_ready = true;
             }
             // wait for a free ring slot and room for the footprint in this half
             int64_t at = -1;
             while (ok) {
-                if (issued - oldest >= K / 2) {
-                    ok = wait_rec(pp + 2 * oldest);
+                if (issued - oldest >= K / NP) {
+                    ok = wait_rec(pp + NP * oldest);
                     ++oldest;
                     continue;
                 }
                 const int live = issued - oldest;
-                at = ring_alloc(dhead, live ? slot_off[(pp + 2 * oldest) % K] - pp * half : 0, live, foot, half);
+                at = ring_alloc(dhead, live ? slot_off[(pp + NP * oldest) % K] - pp * half : 0, live, foot, half);
                 if (at >= 0) break;
-                ok = wait_rec(pp + 2 * oldest);
+                ok = wait_rec(pp + NP * oldest);
                 ++oldest;
             }
             if (!ok) break;
             const int si = rr % K;
             // pull a record ahead into L2 (no shared memory)
-            const int pf = issued + PS_PF / 2;
+            const int pf = issued + PFO;
             const int pj = pf - (issued & ~31);   // index into the two windows
             const uint64_t pf_off = __shfl_sync(0xffffffffu, pj < 32 ? cur_off : nxt_off, pj & 31);
             const uint32_t pf_bytes = __shfl_sync(0xffffffffu, pj < 32 ? cur_bytes : nxt_bytes, pj & 31);
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             __syncwarp();
         }
         // never leave the CTA with copies in flight into its shared memory
-        for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + (pp + 2 * g) % K, uint32_t((pp + 2 * g) / K) & 1u);
+        for (int g = oldest; g < issued; ++g) mbar_wait(full_bar + (pp + NP * g) % K, uint32_t((pp + NP * g) / K) & 1u);
     } else {
         // ========================= compute warps ==============================
         // two groups of PS_NG threads take alternate records (ping-pong).  A
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             double acc[BS];
             // staged slots: all SR with two groups; with three the registers
             // go to the third group and the blocks are read at the products
-            constexpr int SV = G == 2 ? SR : 0;
+            constexpr int SV = (G == 2 || PS_NPROD == 1) ? SR : 0;
             double v[SV > 0 ? SV : 1][BS2] = {};
             // element e of slot u's block of this thread's row (registers, or shared memory)
             auto vblk = [&](int u, int e) -> double {
