@@ -153,6 +153,10 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
         // than two (blocks staged in registers) for every case; BILUK_GROUPS=2
         // selects the two-group kernel
         P.ps.groups = 3;
+        // one producer for large ILU(2)+: its register room stages the blocks
+        // (128^3 ILU(2) 3303 vs 3507 us, 100^3 2138 vs 2192; 64^3 1181 vs 1127,
+        // so small systems keep two); ILU(0) needs both producers (576 vs 714 us)
+        P.ps.nprod = (k >= 2 && n >= 500000) ? 1 : 2;
         if (const char *g = std::getenv("BILUK_GROUPS")) P.ps.groups = std::atoi(g) == 3 ? 3 : 2;
         if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;

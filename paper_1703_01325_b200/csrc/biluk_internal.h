@@ -189,6 +189,7 @@ struct PSweep {
     int64_t xval_ring = 0;           // shared-memory bytes of the fetched-value ring
     int64_t rec_cap = 0, glob_cap = 0;
     int groups = 2;                  // compute groups of the kernel (2 or 3, see psweep.cu)
+    int nprod = 2;                   // producer warps (2, or 1 for ILU(2)+, see psweep.cu)
     int32_t nlrec_max = 0;           // most L records of one part
     std::vector<int32_t> part_rec;   // P+1 record ranges (a part's L records, then its U' records)
     std::vector<PRecInfo> rec;

@@ -344,7 +344,7 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.num_sms = num_sms;
     if (p.engine == 1) {
         p.sweep_ctas = p.ps.P;
-        p.sweep_warps = p.ps.groups * p.ps.nthreads / 32 + 2;   // compute groups + 2 producers
+        p.sweep_warps = p.ps.groups * p.ps.nthreads / 32 + p.ps.nprod;   // compute groups + producers
         p.sweep_stages = PS_KSLOTS;
         p.stage_bytes = p.ps.max_rec;
     } else {

@@ -40,10 +40,8 @@ namespace {
 
 constexpr int PS_NG = 128;            // threads per compute group (= rows per record)
 // compute groups (round-robin over records) are a template parameter G: 2 or 3
-#ifndef PS_NPROD
-#define PS_NPROD 2                    // producer warps (record r served by producer r % PS_NPROD)
-#endif
-constexpr int PS_NAUX = PS_NPROD;     // the producer warps come after the compute groups
+// producer warps (record r served by producer r % NP) are a template
+// parameter NP: 2, or 1 for ILU(2)+ where the freed registers stage blocks
 constexpr int PS_PF = 2;              // records pulled into L2 ahead of their bulk copy (2 measured best of 0-32)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -140,8 +138,8 @@ __device__ __forceinline__ bool mbar_wait_or_abort(uint64_t *bar, uint32_t phase
     return true;
 }
 
-template <int BS, int G>
-__global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(const PSweepArgs a) {
+template <int BS, int G, int NP>
+__global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PSweepArgs a) {
     constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the two producers
     constexpr int BS2 = BS * BS;
     constexpr int VS = ps_vec_stride(BS);
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
     for (int x = tid; x < VS; x += blockDim.x) vring[size_t(x) * RS + a.ring_mask + 1] = 0.0;
     __syncthreads();
 
-    if (warp >= PS_NW && warp < PS_NW + PS_NPROD) {
+    if (warp >= PS_NW && warp < PS_NW + NP) {
         // ============ producers: bulk copies into the record ring ==============
         // producer pp serves records pp, pp+2, ... (the records of compute
         // group pp) in its own half of the ring.  Per record two bulk copies on
@@ -182,7 +180,6 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
         // this part's L sweep is complete).  Space is recycled in record order
         // (empty barriers); records are pulled into L2 ahead so the copies are short.
         const int pp = warp - PS_NW;
-        constexpr int NP = PS_NPROD;
         const int nk = (nrec - pp + NP - 1) / NP;   // records of this producer: pp + NP k
         const uint32_t half = (a.data_bytes / NP) & ~15u;
         unsigned char *ring = dring + pp * half;
@@ -390,7 +387,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * PS_NAUX, 1) psweep_kernel(con
             double acc[BS];
             // staged slots: all SR with two groups; with three the registers
             // go to the third group and the blocks are read at the products
-            constexpr int SV = (G == 2 || PS_NPROD == 1) ? SR : 0;
+            constexpr int SV = (G == 2 || NP == 1) ? SR : 0;
             double v[SV > 0 ? SV : 1][BS2] = {};
             // element e of slot u's block of this thread's row (registers, or shared memory)
             auto vblk = [&](int u, int e) -> double {
@@ -664,10 +661,11 @@ cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s) {
 
 cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s) {
     const size_t smem = psweep_smem_bytes(p);
-    dim3 grid(p.ps.P), block(p.ps.groups * PS_NG + 32 * PS_NAUX);
+    dim3 grid(p.ps.P), block(p.ps.groups * PS_NG + 32 * p.ps.nprod);
 #define PSWEEP_LAUNCH(BS)                                                                                  \
     {                                                                                                      \
-        auto kern = p.ps.groups == 3 ? psweep_kernel<BS, 3> : psweep_kernel<BS, 2>;                        \
+        auto kern = p.ps.groups == 2 ? psweep_kernel<BS, 2, 2>                                             \
+                                     : (p.ps.nprod == 1 ? psweep_kernel<BS, 3, 1> : psweep_kernel<BS, 3, 2>); \
         cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         if (e0 != cudaSuccess) return e0;                                                                  \
         void *args[] = {const_cast<PSweepArgs *>(&a)};                                                     \
@@ -683,10 +681,11 @@ cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm) {
     const size_t smem = psweep_smem_bytes(p);
 #define POCC(BS)                                                                                                  \
     {                                                                                                             \
-        auto kern = p.ps.groups == 3 ? psweep_kernel<BS, 3> : psweep_kernel<BS, 2>;                               \
+        auto kern = p.ps.groups == 2 ? psweep_kernel<BS, 2, 2>                                                    \
+                                     : (p.ps.nprod == 1 ? psweep_kernel<BS, 3, 1> : psweep_kernel<BS, 3, 2>);        \
         cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));      \
         if (e0 != cudaSuccess) return e0;                                                                         \
-        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, p.ps.groups * PS_NG + 32 * PS_NAUX, \
+        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, p.ps.groups * PS_NG + 32 * p.ps.nprod, \
                                                            smem);                                                 \
         if (e0 != cudaSuccess) return e0;                                                                         \
     }
