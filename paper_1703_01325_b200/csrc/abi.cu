@@ -157,6 +157,7 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
         // (128^3 ILU(2) 3303 vs 3507 us, 100^3 2138 vs 2192; 64^3 1181 vs 1127,
         // so small systems keep two); ILU(0) needs both producers (576 vs 714 us)
         P.ps.nprod = (k >= 2 && n >= 500000) ? 1 : 2;
+        if (const char *g = std::getenv("BILUK_NPROD")) P.ps.nprod = std::atoi(g) == 1 ? 1 : 2;
         if (const char *g = std::getenv("BILUK_GROUPS")) P.ps.groups = std::atoi(g) == 3 ? 3 : 2;
         if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;
