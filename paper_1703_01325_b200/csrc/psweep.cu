@@ -385,9 +385,10 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                 }
             };
             double acc[BS];
-            // staged slots: all SR with two groups; with three the registers
-            // go to the third group and the blocks are read at the products
-            constexpr int SV = (G == 2 || NP == 1) ? SR : 0;
+            // staged slots: all SR with two groups or one producer; with three
+            // groups and two producers (128 registers) one slot for b <= 4 and
+            // the other blocks are read at the products
+            constexpr int SV = (G == 2 || NP == 1) ? SR : (BS <= 4 ? 1 : 0);
             double v[SV > 0 ? SV : 1][BS2] = {};
             // element e of slot u's block of this thread's row (registers, or shared memory)
             auto vblk = [&](int u, int e) -> double {
