@@ -49,6 +49,10 @@ BILUK_HD constexpr inline int rows_per_tile(int bs) {
 BILUK_HD constexpr inline int64_t align128(int64_t x) { return (x + 127) & ~int64_t(127); }
 // doubles per position in the sweep vectors (power of two >= bs: vector loads/stores)
 BILUK_HD constexpr inline int vec_stride(int bs) { return bs <= 1 ? 1 : (bs <= 2 ? 2 : (bs <= 4 ? 4 : 8)); }
+// doubles per position of the parity-TAGGED sweep vectors y_t / x_t (both
+// engines): a power of two >= bs + 1, the extra word carrying the values'
+// displaced mantissa LSBs so that published values stay exact (device_util.cuh)
+BILUK_HD constexpr inline int tag_stride(int bs) { return bs < 2 ? 2 : (bs < 4 ? 4 : (bs < 8 ? 8 : 16)); }
 // header: rows int32[R] (natural block-row index, -1 = padding); U' tiles add
 // ypos int32[R] (the row's position in the L sweep, where its y lives)
 BILUK_HD constexpr inline int64_t rec_hdr_bytes(bool upper) { return upper ? 256 : 128; }
@@ -125,7 +129,9 @@ struct Sweep {                       // host copy of one sweep's tile layout
 // contiguous byte range moved by one cp.async.bulk:
 //   hdr   PRecHdr (32 B)
 //   iarr  int32[nrows]          L: the row's U' position (where it stores y for
-//                               the U' sweep); U': natural block row (x scatter)
+//                               the U' sweep); U': natural block row (x scatter);
+//                               bit 31: publish the row to the tagged vector (some
+//                               record fetches it)
 //   desc  int32[S][nrows]       >= 0: vector-ring slot (slot `ring` is zero);
 //                               < 0: fetched dependency -(d+1)
 //   gpos  int32[nglob]          deduplicated dependency positions in the
@@ -137,7 +143,7 @@ struct Sweep {                       // host copy of one sweep's tile layout
 // and, in shared memory only, behind it:
 //   input f64[nrows][pvs]       the rows' own inputs, a second bulk copy of
 //                               the position-ordered b (L) or y (U') vector
-//   deps  f64[bs][nglob]        fetched dependencies, component-major
+//   deps  f64[bs][nglob]        fetched dependencies (exact), component-major
 // ---------------------------------------------------------------------------
 struct PRecHdr {        // 32 bytes
     int32_t nrows, S, nglob;
@@ -163,7 +169,7 @@ struct PRecInfo {       // 64 bytes: one per record, read by the producer, the g
 // doubles per position of the partitioned sweep's vectors (>= 2: 16-byte rows)
 BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
 // fetched dependencies per record (a multiple of 32: one per poll lane and round)
-BILUK_HD constexpr inline int ps_glob_cap(int) { return 1024; }   // fetched dependencies per record (the groups loop over them)
+BILUK_HD constexpr inline int ps_glob_cap(int) { return 1024; }   // fetched dependencies per record (the compute threads loop over them)
 constexpr int PS_KSLOTS = 16;      // records in flight per CTA (mbarrier sets)
 
 // an assignment of block rows to parts (any assignment is deadlock-free:
@@ -183,15 +189,16 @@ struct PSweep {
     int32_t partition = 0;           // Partition::kind
     int64_t grid[3] = {0, 0, 0};
     int32_t split[2] = {0, 0};
-    int32_t nthreads = 128;          // compute threads per CTA (+ one prefetch warp)
+    int32_t nthreads = 128;          // rows per record at most = threads of a compute group
     int32_t ring = 1024;             // vector ring rows (power of two; slot `ring` is all zeros)
     int64_t data_ring = 0;           // shared-memory bytes of the record ring
     int64_t xval_ring = 0;           // shared-memory bytes of the fetched-value ring
     int64_t rec_cap = 0, glob_cap = 0;
-    int groups = 2;                  // compute groups of the kernel (2 or 3, see psweep.cu)
-    int nprod = 2;                   // producer warps (2, or 1 for ILU(2)+, see psweep.cu)
+    int groups = 3;                  // compute groups of the sweep kernel (2 or 3, see psweep.cu)
+    int nprod = 2;                   // producer warps of the sweep kernel (1 or 2, see psweep.cu)
     int32_t nlrec_max = 0;           // most L records of one part
-    std::vector<int32_t> part_rec;   // P+1 record ranges (a part's L records, then its U' records)
+    std::vector<int32_t> part_rec;   // P+1 record ranges (a part's L records, then its U' records),
+                                     // then P counts of L records
     std::vector<PRecInfo> rec;
     std::vector<int32_t> idx;        // compact index sections
     std::vector<int32_t> vmap;       // value maps
@@ -259,10 +266,8 @@ inline int64_t plan_npos(const Plan &p) {
     const int64_t m = a > b ? a : b;
     return m > p.n ? m : p.n;
 }
-// doubles per position of the sweep vectors y_t / x_t (either engine)
-inline int plan_vs(const Plan &p) {
-    return p.engine == 1 ? ps_vec_stride(p.bs) : vec_stride(p.bs);
-}
+// doubles per position of the tagged sweep vectors y_t / x_t (either engine)
+inline int plan_vs(const Plan &p) { return tag_stride(p.bs); }
 
 // host planner (plan.cpp)
 int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,

@@ -78,23 +78,88 @@ __device__ __forceinline__ void st_row(double *p, const double (&v)[BS]) {
     }
 }
 
-// ---- parity tags.  Every value a sweep publishes carries the apply epoch's
-// parity in its mantissa LSB (<= 1 ulp, 2^-52 relative).  A consumer polls the
-// value itself: the value is its own ready flag, so a dependency costs ONE
-// L2 round trip and no fences; no reset pass is needed because every element
-// is rewritten exactly once per apply and the parity alternates.
-__device__ __forceinline__ double tag(double v, uint32_t par) {
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-    b = (b & ~1ull) | par;
-    return __longlong_as_double(static_cast<long long>(b));
-}
+// ---- parity tags.  Every word a sweep publishes carries the apply epoch's
+// parity in its LSB.  A consumer polls the words themselves: each is its own
+// ready flag, so a dependency costs ONE L2 round trip and no fences; no reset
+// pass is needed because every row is rewritten exactly once per apply and the
+// parity alternates.  A TAGGED ROW is exact: words 0..BS-1 hold the values with
+// their LSB replaced by the tag, word BS holds the BS displaced LSBs (bits
+// 1..BS) and the tag (bit 0); tag_stride(BS) >= BS + 1 words per row.
 __device__ __forceinline__ uint32_t tag_of(double v) {
     return static_cast<uint32_t>(__double_as_longlong(v)) & 1u;
 }
-// consumers clear the tag bit, so what they compute with does not depend on
-// the epoch's parity: results are bitwise identical from apply to apply
-__device__ __forceinline__ double untag(double v) {
-    return __longlong_as_double(__double_as_longlong(v) & ~1ll);
+__device__ __forceinline__ double bits_as_double(unsigned long long b) {
+    return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ unsigned long long double_bits(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+// the BS + 1 tagged words of a row
+template <int BS>
+__device__ __forceinline__ void tag_row(const double (&v)[BS], uint32_t par, double (&w)[BS + 1]) {
+    unsigned long long lsb = par;
+#pragma unroll
+    for (int c = 0; c < BS; ++c) {
+        const unsigned long long b = double_bits(v[c]);
+        lsb |= (b & 1ull) << (c + 1);
+        w[c] = bits_as_double((b & ~1ull) | par);
+    }
+    w[BS] = bits_as_double(lsb);
+}
+template <int BS>
+__device__ __forceinline__ bool row_ready(const double (&w)[BS + 1], uint32_t par) {
+    uint32_t ok = 1;
+#pragma unroll
+    for (int c = 0; c <= BS; ++c) ok &= (tag_of(w[c]) == par);
+    return ok != 0;
+}
+// the exact values of a ready row
+template <int BS>
+__device__ __forceinline__ void untag_row(const double (&w)[BS + 1], double (&v)[BS]) {
+    const unsigned long long lsb = double_bits(w[BS]);
+#pragma unroll
+    for (int c = 0; c < BS; ++c) v[c] = bits_as_double((double_bits(w[c]) & ~1ull) | ((lsb >> (c + 1)) & 1ull));
+}
+// N consecutive doubles at p (32-byte aligned when N >= 3, 16-byte when N == 2),
+// relaxed gpu-scope, the fewest vector accesses; N = 3 is read/written as 4
+// (the 4th word belongs to the same row's padding)
+template <int N>
+__device__ __forceinline__ void ld_words(const double *p, double (&w)[N]) {
+    constexpr int N4 = N / 4, R = N - 4 * N4;
+#pragma unroll
+    for (int k = 0; k < N4; ++k) ld_relaxed_v4(p + 4 * k, w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    if constexpr (R == 3) {
+        double d;
+        ld_relaxed_v4(p + 4 * N4, w[4 * N4], w[4 * N4 + 1], w[4 * N4 + 2], d);
+    } else if constexpr (R == 2) {
+        ld_relaxed_v2(p + 4 * N4, w[4 * N4], w[4 * N4 + 1]);
+    } else if constexpr (R == 1) {
+        w[4 * N4] = ld_relaxed(p + 4 * N4);
+    }
+}
+template <int N>
+__device__ __forceinline__ void st_words(double *p, const double (&w)[N]) {
+    constexpr int N4 = N / 4, R = N - 4 * N4;
+#pragma unroll
+    for (int k = 0; k < N4; ++k) st_relaxed_v4(p + 4 * k, w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    if constexpr (R == 3) {
+        st_relaxed_v4(p + 4 * N4, w[4 * N4], w[4 * N4 + 1], w[4 * N4 + 2], 0.0);
+    } else if constexpr (R == 2) {
+        st_relaxed_v2(p + 4 * N4, w[4 * N4], w[4 * N4 + 1]);
+    } else if constexpr (R == 1) {
+        st_relaxed(p + 4 * N4, w[4 * N4]);
+    }
+}
+// publish / poll one tagged row (tag_stride(BS) doubles at p)
+template <int BS>
+__device__ __forceinline__ void st_tagged(double *p, const double (&v)[BS], uint32_t par) {
+    double w[BS + 1];
+    tag_row<BS>(v, par, w);
+    st_words<BS + 1>(p, w);
+}
+template <int BS>
+__device__ __forceinline__ void ld_tagged(const double *p, double (&w)[BS + 1]) {
+    ld_words<BS + 1>(p, w);
 }
 
 // ---- mbarrier + bulk async copy (cp.async.bulk, the 1-D TMA path)

@@ -325,7 +325,7 @@ __global__ void pack_ell_kernel(int64_t n, int64_t ntiles, const TileMeta *__res
 // chain; only the vector values travel along it.  A lane owns one block row:
 //   L :  y_i = b_i - sum_j L_ij y_j
 //   U':  x_i = D_i^-1 y_i - sum_j U'_ij x_j
-// Dependencies are polled directly on the parity-tagged values (see tag()),
+// Dependencies are polled directly on the parity-tagged rows (see tag_row()),
 // ONE component per dependency until it is published, then the rest.  To keep
 // the polls from flooding L2, a warp first waits (one load per warp, with
 // back-off) until every level <= its own level - gap is complete: per-level
@@ -353,13 +353,13 @@ __device__ __forceinline__ bool timed_out(uint64_t &t0, uint32_t &spins, const S
 // p[e] + q * stride.  Every poll round issues ALL pending loads before
 // looking at any of them, so one round costs one L2 round trip however many
 // dependencies a row has (checking each value right after its own load would
-// serialise one round trip per dependency).  Values come back untagged.
+// serialise one round trip per dependency).  Values come back exact (untag_row).
 template <int BS, int NE>
 __device__ __forceinline__ void wait_values(const double *__restrict__ base, const double *__restrict__ last_base,
                                             const int (&pos)[NE], double (&xv)[NE][BS], uint32_t pend, uint32_t par,
                                             const SweepArgs &a) {
     // entry e < NE-1 is the row at position pos[e] of base, the last entry of last_base;
-    // a row is vec_stride(BS) contiguous doubles
+    // a row is tag_stride(BS) contiguous doubles
     uint64_t t0 = 0;
     uint32_t spins = 0;
 #pragma unroll
@@ -367,28 +367,22 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ base, con
 #pragma unroll
         for (int q = 0; q < BS; ++q) xv[e][q] = 0.0;   // entries never polled contribute zero
     while (pend) {
+        uint32_t still = 0;
 #pragma unroll
         for (int e = 0; e < NE; ++e)
             if (pend & (1u << e)) {
-                ld_row<BS>((e == NE - 1 ? last_base : base) + int64_t(pos[e]) * vec_stride(BS), xv[e]);
+                double w[BS + 1];
+                ld_tagged<BS>((e == NE - 1 ? last_base : base) + int64_t(pos[e]) * tag_stride(BS), w);
+                if (row_ready<BS>(w, par))
+                    untag_row<BS>(w, xv[e]);
+                else
+                    still |= 1u << e;
             }
-        uint32_t still = 0;
-#pragma unroll
-        for (int e = 0; e < NE; ++e) {
-            uint32_t ok = 1;
-#pragma unroll
-            for (int q = 0; q < BS; ++q) ok &= (tag_of(xv[e][q]) == par);
-            if (!ok) still |= 1u << e;
-        }
         pend &= still;
         if (!pend) break;
         if (timed_out(t0, spins, a)) break;
         if (a.fine_sleep_ns) __nanosleep(a.fine_sleep_ns);
     }
-#pragma unroll
-    for (int e = 0; e < NE; ++e)
-#pragma unroll
-        for (int q = 0; q < BS; ++q) xv[e][q] = untag(xv[e][q]);
 }
 
 // the finisher of a level tries to advance the completed-level prefix
@@ -580,8 +574,8 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
         // not flood their SM's load pipeline with full-warp polls
         const int probe = a.probe == 1 ? m.probe[0] : (a.probe == 2 ? m.probe[1] : -1);
         if (lane == 0 && probe != -1) {
-            const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + int64_t(probe) * vec_stride(BS) + (BS - 1)
-                                          : a.y_t + int64_t(-probe - 2) * vec_stride(BS) + (BS - 1);
+            const double *pv = probe >= 0 ? (up ? a.x_t : a.y_t) + int64_t(probe) * tag_stride(BS) + BS
+                                          : a.y_t + int64_t(-probe - 2) * tag_stride(BS) + BS;
             uint64_t t0 = 0;
             uint32_t spins = 0;
             while (tag_of(ld_relaxed(pv)) != par) {
@@ -603,11 +597,8 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
             if (a.trace && lane == 0) cyc_fma = clock64();
             // publish the row at its own position: one (or two) vector stores,
             // coalesced across the warp's consecutive positions
-            double *dst = (up ? a.x_t : a.y_t) + ((up ? t - a.nl : t) * R + lane) * vec_stride(BS);
-            double pub[BS];
-#pragma unroll
-            for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
-            st_row<BS>(dst, pub);
+            double *dst = (up ? a.x_t : a.y_t) + ((up ? t - a.nl : t) * R + lane) * tag_stride(BS);
+            st_tagged<BS>(dst, acc, par);
             if (up && a.out) {
 #pragma unroll
                 for (int r = 0; r < BS; ++r) a.out[int64_t(row) * BS + r] = acc[r];

@@ -41,9 +41,9 @@ struct SweepArgs {
 struct PSweepArgs {
     const PRecInfo *rec;         // all records (a CTA's range: part_rec[c] .. part_rec[c+1])
     const unsigned char *recs;   // record bytes
-    const int32_t *part_rec;     // P+1
+    const int32_t *part_rec;     // P+1 record ranges, then P counts of L records
     const double *b;             // right-hand side (n*bs, natural order)
-    double *y_t;                 // parity-tagged y at L positions (vec_stride(bs) doubles each)
+    double *y_t;                 // parity-tagged y at L positions (tag_stride(bs) doubles each)
     double *x_t;                 // parity-tagged x at U' positions
     double *out;                 // untagged x (natural order; may be null)
     DevStatus *st;

@@ -19,10 +19,13 @@
 //     fetched values), forms the products and publishes the row to the ring,
 //     to the tagged global vector (other parts poll it) and to y_u (L, the
 //     U' input) or the caller's x (U').
-//   * two PRODUCER warps (even / odd records, each in its half of the data
-//     ring) stream records and their rows' inputs (b_perm / y_u, position
-//     ordered) into shared memory with cp.async.bulk on mbarriers, pulling
-//     records ahead into L2 with cp.async.bulk.prefetch.L2.
+//   * NP PRODUCER warps (record r served by producer r % NP, each in its
+//     share of the data ring) stream records and their rows' inputs (b_perm /
+//     y_u, position ordered) into shared memory with cp.async.bulk on
+//     mbarriers, pulling records ahead into L2 with cp.async.bulk.prefetch.L2.
+// Published rows go to the part's vector ring, to the parity-tagged global
+// vector (only rows some record fetches: iarr bit 31) as exact tagged rows
+// (tag_row), and to y_u (L) / the caller's x (U').
 // Every CTA walks its rows in global level order, L then U', and every
 // dependency has a lower level, so the CTA holding the lowest unfinished row
 // is never blocked -- for any row-to-part assignment (no deadlock).
@@ -43,6 +46,7 @@ constexpr int PS_NG = 128;            // threads per compute group (= rows per r
 // producer warps (record r served by producer r % NP) are a template
 // parameter NP: 2, or 1 for ILU(2)+ where the freed registers stage blocks
 constexpr int PS_PF = 2;              // records pulled into L2 ahead of their bulk copy (2 measured best of 0-32)
+constexpr uint32_t PS_PUB = 0x80000000u;   // iarr bit: publish the row to the tagged vector
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -101,9 +105,6 @@ __device__ __forceinline__ bool ps_timed_out(uint64_t &t0, uint32_t &spins, cons
 
 }  // namespace
 
-__device__ __forceinline__ void cp_async_8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async_16(void *dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
@@ -142,12 +143,14 @@ template <int BS, int G, int NP>
 __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PSweepArgs a) {
     constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the two producers
     constexpr int BS2 = BS * BS;
-    constexpr int VS = ps_vec_stride(BS);
+    constexpr int VS = ps_vec_stride(BS);   // input rows (b gathered / y_u)
+    constexpr int TVS = tag_stride(BS);     // tagged rows of y_t / x_t
     constexpr int K = PS_KSLOTS;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[K];    // record bytes + inputs landed (two bulk copies)
     __shared__ __align__(8) uint64_t empty_bar[K];   // record consumed (every thread of a compute group)
     __shared__ uint32_t slot_off[K];
+    __shared__ __align__(8) uint64_t ldone_bar;      // every compute thread is past its last L record
     __shared__ int abort_flag;   // a wait timed out somewhere (the device status is sticky)
     __shared__ int last_cta;
     if (a.skip_flag && ld_relaxed_s32(a.skip_flag) != 0) return;
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
     double *vring = reinterpret_cast<double *>(smem);
     unsigned char *dring = smem + size_t(a.ring_mask + 2) * VS * 8;
     const int r0 = a.part_rec[blockIdx.x], nrec = a.part_rec[blockIdx.x + 1] - r0;
+    const int nlrec = a.part_rec[gridDim.x + 1 + blockIdx.x];   // L records come first
     const uint32_t par = ld_relaxed_u32(&a.st->epoch) & 1u;
 
     if (tid == 0) {
@@ -163,6 +167,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             mbar_init(full_bar + s, 1);
             mbar_init(empty_bar + s, PS_NG);
         }
+        mbar_init(&ldone_bar, G * PS_NG);
         abort_flag = 0;
         fence_mbar_init();
     }
@@ -172,13 +177,13 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
     __syncthreads();
 
     if (warp >= PS_NW && warp < PS_NW + NP) {
-        // ============ producers: bulk copies into the record ring ==============
-        // producer pp serves records pp, pp+2, ... (the records of compute
-        // group pp) in its own half of the ring.  Per record two bulk copies on
-        // one mbarrier: the record's bytes and its rows' inputs (positions
-        // pos0 .. pos0+nr of b_perm for L, of y_u for U' -- the latter only once
-        // this part's L sweep is complete).  Space is recycled in record order
-        // (empty barriers); records are pulled into L2 ahead so the copies are short.
+        // ============ producers: records into the data ring ==================
+        // producer pp serves records pp, pp+NP, ... in its own share of the
+        // ring.  Per record two bulk copies on one mbarrier: the record's bytes
+        // and its rows' inputs (positions pos0 .. pos0+nr of b_perm for L, of
+        // y_u for U' -- the latter only once this part's L sweep is complete).
+        // Space is recycled in record order (empty barriers); records are
+        // pulled into L2 ahead so the copies are short.
         const int pp = warp - PS_NW;
         const int nk = (nrec - pp + NP - 1) / NP;   // records of this producer: pp + NP k
         const uint32_t half = (a.data_bytes / NP) & ~15u;
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             pos0u = uint32_t(ri.pos0) | (uint32_t(ri.level & 1) << 31);
             nr = uint32_t(ri.nrows);
         };
-        auto wait_rec = [&](int rr) -> bool {   // record rr (any parity) consumed
+        auto wait_rec = [&](int rr) -> bool {   // own record rr consumed
             return mbar_wait_or_abort(empty_bar + rr % K, uint32_t(rr / K) & 1u, &abort_flag, a);
         };
         if (lane < nk) fetch(lane, cur_off, cur_bytes, cur_foot, cur_pm, cur_nr);
@@ -228,10 +233,11 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const int rr = pp + NP * issued;   // record index
             bool ok = true;
             if (up && !up_ready) {
-                // y_u is written by this part's L sweep: every L record of both
-                // groups must be consumed before the first U' input copy
-                for (; ok && oldest < issued; ++oldest) ok = wait_rec(pp + NP * oldest);
-                if (ok && rr >= 1) ok = wait_rec(rr - 1);
+                // y_u is written by this part's L sweep (generic proxy): every
+                // compute thread issues fence.proxy.async after its last L
+                // record and then arrives on ldone_bar, so this wait orders
+                // every y_u store before the U' input bulk copies
+                ok = mbar_wait_or_abort(&ldone_bar, 0u, &abort_flag, a);
                 up_ready = true;
             }
             // wait for a free ring slot and room for the footprint in this half
@@ -255,9 +261,9 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const int pj = pf - (issued & ~31);   // index into the two windows
             const uint64_t pf_off = __shfl_sync(0xffffffffu, pj < 32 ? cur_off : nxt_off, pj & 31);
             const uint32_t pf_bytes = __shfl_sync(0xffffffffu, pj < 32 ? cur_bytes : nxt_bytes, pj & 31);
+            const uint32_t in_bytes = nr * uint32_t(VS * 8);
             if (lane == 0) {
                 slot_off[si] = uint32_t(at) + pp * half;
-                const uint32_t in_bytes = nr * uint32_t(VS * 8);
                 mbar_expect_tx(full_bar + si, bytes + in_bytes);
                 bulk_g2s(ring + at, a.recs + off, bytes, full_bar + si, pol);
                 bulk_g2s(ring + at + bytes, (up ? a.y_u : a.b_perm) + size_t(pos0) * VS, in_bytes, full_bar + si, pol);
@@ -284,10 +290,22 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
         const uint32_t vring_s = 0;   // the vector ring starts the dynamic shared memory
         auto lds = [&](uint32_t off) -> double { return *reinterpret_cast<const double *>(smem + off); };
         auto sts = [&](uint32_t off, double v) { *reinterpret_cast<double *>(smem + off) = v; };
+        bool ldone = false;   // arrived on ldone_bar (once per thread, before its first U' record)
+        auto arrive_ldone = [&]() {
+            fence_proxy_async_global();   // this thread's y_u stores, before the U' input bulk copies
+            mbar_arrive(&ldone_bar);
+            ldone = true;
+        };
         for (int i = grp; i < nrec; i += G) {
             const int s = i % K;
             const uint32_t ph = uint32_t(i / K) & 1u;
-            if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) break;
+            if (!ldone && i >= nlrec) arrive_ldone();
+            if (!mbar_wait_or_abort(full_bar + s, ph, &abort_flag, a)) {
+                // aborted: still pass the hand-over on, so no group waits forever
+                if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);
+                if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % G, 2 * PS_NG);
+                break;
+            }
             // clock64 stamps of the stages for the first 16384 records (trace debug rows)
             unsigned long long *dbg =
                 (a.trace && gt == 0 && r0 + i < 16384) ? a.trace + size_t(a.nrec_total + r0 + i) * 8 : nullptr;
@@ -312,8 +330,8 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const int32_t *gpos = desc + size_t(S) * nr;
             const double *gvec = up ? a.x_t : a.y_t;
             const bool dneed = gt < ng;
-            double dval[BS];
-            if (dneed) ld_row<BS>(gvec + size_t(gpos[gt]) * VS, dval);
+            double dval[BS + 1];
+            if (dneed) ld_tagged<BS>(gvec + size_t(gpos[gt]) * TVS, dval);
             // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
             auto init_acc = [&](int q, double (&acc)[BS]) {
                 const double *inp = inp0 + size_t(q) * VS;
@@ -365,14 +383,12 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             };
             // publish row q: the ring (this part's next levels), the tagged
             // global vector (other parts) and y_u (L) / the caller's x (U')
-            auto publish = [&](int q, int idx, const double (&acc)[BS]) {
+            auto publish = [&](int q, uint32_t iv, const double (&acc)[BS]) {
                 const uint32_t rs = vring_s + uint32_t((h.seq0 + q) & a.ring_mask) * 8u;
 #pragma unroll
                 for (int r = 0; r < BS; ++r) sts(rs + uint32_t(r) * uint32_t(RS) * 8u, acc[r]);
-                double pub[BS];
-#pragma unroll
-                for (int r = 0; r < BS; ++r) pub[r] = tag(acc[r], par);
-                st_row<BS>((up ? a.x_t : a.y_t) + size_t(h.pos0 + q) * VS, pub);
+                if (iv & PS_PUB) st_tagged<BS>((up ? a.x_t : a.y_t) + size_t(h.pos0 + q) * TVS, acc, par);
+                const uint32_t idx = iv & ~PS_PUB;
                 if (up) {
                     if (a.out) {
 #pragma unroll
@@ -396,7 +412,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             };
             uint32_t xa[SR];   // shared address of component 0 of each staged dependency
             uint32_t xs[SR];   // its component stride in bytes
-            int idx = 0;   // L: the row's U' position; U': its natural row
+            uint32_t idx = 0;   // iarr entry: L: the row's U' position; U': its natural row (| PS_PUB)
             // rows longer than the staged slots in a record of few rows: TPR
             // threads per row share its slots (strided) and sum by shuffles,
             // so the idle threads of a short record shorten the chain
@@ -407,11 +423,11 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
 #pragma unroll
                 for (int r = 0; r < BS; ++r) acc[r] = 0.0;
                 if (tlive && tj == 0) {
-                    idx = iarr[tq];
+                    idx = uint32_t(iarr[tq]);
                     init_acc(tq, acc);
                 }
             } else if (live) {
-                idx = iarr[gt];
+                idx = uint32_t(iarr[gt]);
                 init_acc(gt, acc);
 #pragma unroll
                 for (int u = 0; u < SR; ++u) {
@@ -425,28 +441,26 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             }
             if (dbg) dbg[1] = clock64();
             {
-                auto fetch_dep = [&](int e, double (&dv)[BS], bool loaded) {
-                    const double *src = gvec + size_t(gpos[e]) * VS;
-                    if (!loaded) ld_row<BS>(src, dv);
+                auto fetch_dep = [&](int e, double (&dv)[BS + 1], bool loaded) {
+                    const double *src = gvec + size_t(gpos[e]) * TVS;
+                    if (!loaded) ld_tagged<BS>(src, dv);
                     uint64_t t0 = 0;
                     uint32_t spins = 0;
-                    while (true) {
-                        uint32_t ok = 1;
-#pragma unroll
-                        for (int q = 0; q < BS; ++q) ok &= (tag_of(dv[q]) == par);
-                        if (ok) break;
+                    while (!row_ready<BS>(dv, par)) {
                         if (ps_timed_out(t0, spins, a)) {
-                            abort_flag = 1;
+                            *reinterpret_cast<volatile int *>(&abort_flag) = 1;
                             break;
                         }
-                        ld_row<BS>(src, dv);
+                        ld_tagged<BS>(src, dv);
                     }
+                    double v[BS];
+                    untag_row<BS>(dv, v);
 #pragma unroll
-                    for (int q = 0; q < BS; ++q) sts(dep_s + uint32_t(q * ng + e) * 8u, untag(dv[q]));
+                    for (int q = 0; q < BS; ++q) sts(dep_s + uint32_t(q * ng + e) * 8u, v[q]);
                 };
                 if (dneed) fetch_dep(gt, dval, true);
                 for (int e = gt + PS_NG; e < ng; e += PS_NG) {
-                    double dv2[BS];
+                    double dv2[BS + 1];
                     fetch_dep(e, dv2, false);
                 }
                 if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 3] = globaltimer();
@@ -457,7 +471,10 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             // the other group has published record i-1
             if (i > 0) named_bar_sync(1 + grp, 2 * PS_NG);   // arrive of record i-1's group
             if (dbg) dbg[3] = clock64();
-            if (*reinterpret_cast<volatile int *>(&abort_flag)) break;
+            if (*reinterpret_cast<volatile int *>(&abort_flag)) {
+                if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % G, 2 * PS_NG);   // pass it on
+                break;
+            }
             if (tpr > 1) {
                 if (tlive) {
                     for (int u = tj; u < S; u += tpr) {
@@ -517,9 +534,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                 if (dbg) dbg[5] = clock64();
             }
             // hand record i+1 to the next group, release record i's ring space
-            // (an L record's y_u stores are read later by the async proxy)
             if (i + 1 < nrec) named_bar_arrive(1 + (grp + 1) % G, 2 * PS_NG);
-            if (!up) fence_proxy_async_global();
             if (dbg) dbg[6] = clock64();
             mbar_arrive(empty_bar + s);
             if (dbg) dbg[7] = clock64();
@@ -531,6 +546,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                 a.trace[size_t(r0 + i) * 8 + 7] = uint64_t(uint32_t(h.flags));
             }
         }
+        if (!ldone) arrive_ldone();
     }
     // the last CTA to finish advances the epoch (every CTA read it at entry)
     __syncthreads();
@@ -595,7 +611,7 @@ __global__ void ppack_kernel(int64_t nrec, const PRecInfo *__restrict__ info, co
             const int32_t *rows = src + sizeof(PRecHdr) / 4;
             for (int e = lane; e < BS2 * nr; e += 32) {
                 const int el = e / nr, q = e - el * nr;
-                vals[e] = dinv[int64_t(rows[q]) * BS2 + el];
+                vals[e] = dinv[int64_t(uint32_t(rows[q]) & ~PS_PUB) * BS2 + el];
             }
             vals += int64_t(BS2) * nr;
         }

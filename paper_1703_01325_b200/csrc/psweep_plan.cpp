@@ -34,7 +34,7 @@ inline int64_t rec_total_bytes(int bs2, int nrows, int S, int nglob, bool upper)
     return a16(rec_vals_off(nrows, S, nglob, upper) + 8 * int64_t(bs2) * nrows * (S + (upper ? 1 : 0)));
 }
 // shared-memory footprint: the streamed bytes, the inputs (vs doubles per
-// row) and the fetched dependencies (bs doubles each)
+// row) and the fetched dependencies (bs doubles each, exact)
 inline int64_t rec_foot_bytes(int bs2, int vs, int nrows, int S, int nglob, bool upper) {
     const int bs = int(std::lround(std::sqrt(double(bs2))));
     return rec_total_bytes(bs2, nrows, S, nglob, upper) + int64_t(nrows) * vs * 8 + a16(int64_t(nglob) * bs * 8);
@@ -292,7 +292,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     ps.split[0] = pt.split[0];
     ps.split[1] = pt.split[1];
     // ---- shared-memory budget of one CTA ---------------------------------------
-    ps.nthreads = 128;
+    ps.nthreads = 128;   // rows per record = threads of a compute group
     ps.ring = bs <= 4 ? 512 : 256;
     const int64_t vring = int64_t(ps.ring + 2) * vs * 8;
     ps.xval_ring = 0;   // fetched values live in each record's footprint
@@ -316,6 +316,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     ps.idx.clear();
     ps.vmap.clear();
     ps.part_rec.assign(P + 1, 0);
+    std::vector<int32_t> part_nl(P, 0);   // L records of each part
     ps.rec_total = ps.max_rec = ps.max_glob = ps.nglob_total = 0;
     ps.nlrec_max = 0;
     const int32_t mask = ps.ring - 1;
@@ -457,11 +458,40 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
                 ps.rec.push_back(info);
                 ++ci0;
             }
-            if (!up) ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
+            if (!up) {
+                ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
+                part_nl[c] = int32_t(ps.rec.size() - rec_begin);
+            }
         }
     }
     ps.part_rec[P] = int32_t(ps.rec.size());
+    ps.part_rec.insert(ps.part_rec.end(), part_nl.begin(), part_nl.end());   // then P L-record counts
     if (ps.rec.size() >= size_t(INT32_MAX)) return fail(BILUK_EUNSUPPORTED, "too many sweep records");
+    // a row is published to the tagged global vector only if some record
+    // fetches it (other parts, or rows that left the ring): mark it in iarr
+    {
+        std::vector<uint8_t> need[2] = {std::vector<uint8_t>(n, 0), std::vector<uint8_t>(n, 0)};
+        for (const PRecInfo &ri : ps.rec) {
+            const int32_t *gp = ps.idx.data() + ri.idx_off + sizeof(PRecHdr) / 4 + int64_t(ri.nrows) * (1 + ri.S);
+            for (int t = 0; t < ri.nglob; ++t) need[ri.level & 1][gp[t]] = 1;
+        }
+        for (const PRecInfo &ri : ps.rec) {
+            int32_t *iarr = ps.idx.data() + ri.idx_off + sizeof(PRecHdr) / 4;
+            for (int q = 0; q < ri.nrows; ++q)
+                if (need[ri.level & 1][ri.pos0 + q]) iarr[q] = int32_t(uint32_t(iarr[q]) | 0x80000000u);
+        }
+    }
+    // fault injection (tests only): the first record that fetches a
+    // dependency instead waits on its own first row, which is published after
+    // it -- the sweep must time out with BILUK_ETIMEOUT, not hang
+    if (const char *env = std::getenv("BILUK_FAULT_GPOS")) {
+        if (std::atoi(env) == 1)
+            for (const PRecInfo &ri : ps.rec)
+                if (ri.nglob > 0) {
+                    ps.idx[ri.idx_off + sizeof(PRecHdr) / 4 + int64_t(ri.nrows) * (1 + ri.S)] = ri.pos0;
+                    break;
+                }
+    }
     return BILUK_OK;
 }
 
