@@ -106,7 +106,10 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
 /* apply_preconditioner(f, b) -- trisolve.py:169-182 (Alg. 7):
  * x = U'^{-1} D^{-1} L^{-1} b, one persistent sync-free kernel for both
  * sweeps.  dev_b and dev_x hold n*bs doubles; dev_x may not alias dev_b.
- * Asynchronous; a dependency-wait timeout is reported by biluk_plan_status. */
+ * Asynchronous; a dependency-wait timeout is reported by biluk_plan_status.
+ * Applies of one plan share its device workspace, so they run one at a time:
+ * an apply issued on a different stream than the previous one first waits
+ * (cudaStreamWaitEvent) for that previous apply.  Plans are independent. */
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream);
 
 /* Diagnostics: CUDA events around the sweep launch of every subsequent apply

@@ -279,11 +279,27 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
     return BILUK_OK;
 }
 
+static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream);
+
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream) {
     if (!plan || !plan->p.factored) return fail(BILUK_EARG, "plan is not factored");
     Plan &p = plan->p;
     if (p.n == 0) return BILUK_OK;
     if (dev_b == dev_x) return fail(BILUK_EARG, "output may not alias the right-hand side");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // applies of one plan share its workspace (tagged vectors, epoch): order an
+    // apply on a new stream after the previous one
+    if (plan->last_ev && plan->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, plan->last_ev, 0), "apply");
+    int rc = apply_launch(plan, dev_b, dev_x, st);
+    if (rc != BILUK_OK) return rc;
+    if (!plan->last_ev) CUDA_TRY(cudaEventCreateWithFlags(&plan->last_ev, cudaEventDisableTiming), "apply");
+    CUDA_TRY(cudaEventRecord(plan->last_ev, st), "apply");
+    plan->last_stream = st;
+    return BILUK_OK;
+}
+
+static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream) {
+    Plan &p = plan->p;
     if (p.engine == 1) {
         PSweepArgs a{};
         a.rec = reinterpret_cast<const PRecInfo *>(p.ws + p.off.ps_info);

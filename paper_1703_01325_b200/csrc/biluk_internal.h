@@ -290,9 +290,14 @@ struct biluk_plan {
     biluk::Plan p;
     // optional CUDA events around the sweep launch (biluk_plan_set_timing)
     cudaEvent_t tev[2] = {nullptr, nullptr};
+    // the last apply's completion and stream: an apply on another stream waits
+    // for it, because every apply of a plan uses the plan's sweep workspace
+    cudaEvent_t last_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
     ~biluk_plan() {
         for (cudaEvent_t e : tev)
             if (e) cudaEventDestroy(e);
+        if (last_ev) cudaEventDestroy(last_ev);
     }
 };
 struct biluk_op {

@@ -241,6 +241,7 @@ struct Ctx {
     double *partials;
     int grid;
     cudaError_t err = cudaSuccess;
+    int prc = BILUK_OK;   // the preconditioner's own status when it failed (plan apply or callback)
     // batched solves (biluk_bicgstab_batched); defaults describe one system
     int nsys = 1;
     const int64_t *seg = nullptr;
@@ -317,12 +318,17 @@ int biluk::Ctx::apply(const double *b, double *x) {
         err = cudaMemcpyAsync(x, b, 8 * len, cudaMemcpyDeviceToDevice, s);
         return err ? BILUK_ECUDA : BILUK_OK;
     }
-    if (rc != BILUK_OK) err = cudaErrorUnknown;
+    if (rc != BILUK_OK) {
+        prc = rc;
+        err = cudaErrorUnknown;
+    }
     return rc;
 }
 
 static int krylov_fail(Ctx &c, const char *what) {
-    if (c.err == cudaErrorUnknown) return BILUK_ECUDA;   // preconditioner already set the message
+    // the preconditioner already set the message: pass its status on (e.g.
+    // BILUK_EARG from a callback that returned a wrong-length vector)
+    if (c.err == cudaErrorUnknown) return c.prc != BILUK_OK ? c.prc : BILUK_ECUDA;
     if (c.err != cudaSuccess)
         return fail(BILUK_ECUDA, std::string(what) + ": " + cudaGetErrorString(c.err));
     return BILUK_OK;

@@ -676,39 +676,46 @@ cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// the kernel instantiation of a plan: compute groups x producer warps
+template <int BS>
+static const void *psweep_fn(int groups, int nprod) {
+    if (groups == 2)
+        return nprod == 1 ? reinterpret_cast<const void *>(psweep_kernel<BS, 2, 1>)
+                          : reinterpret_cast<const void *>(psweep_kernel<BS, 2, 2>);
+    return nprod == 1 ? reinterpret_cast<const void *>(psweep_kernel<BS, 3, 1>)
+                      : reinterpret_cast<const void *>(psweep_kernel<BS, 3, 2>);
+}
+
+static cudaError_t psweep_kernel_of(const Plan &p, const void **fn) {
+#define PSWEEP_FN(BS) *fn = psweep_fn<BS>(p.ps.groups, p.ps.nprod);
+    BILUK_BS_DISPATCH(p.bs, PSWEEP_FN)
+#undef PSWEEP_FN
+    return cudaSuccess;
+}
+
+static int psweep_threads(const Plan &p) { return p.ps.groups * PS_NG + 32 * p.ps.nprod; }
+
 cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s) {
     const size_t smem = psweep_smem_bytes(p);
-    dim3 grid(p.ps.P), block(p.ps.groups * PS_NG + 32 * p.ps.nprod);
-#define PSWEEP_LAUNCH(BS)                                                                                  \
-    {                                                                                                      \
-        auto kern = p.ps.groups == 2 ? psweep_kernel<BS, 2, 2>                                             \
-                                     : (p.ps.nprod == 1 ? psweep_kernel<BS, 3, 1> : psweep_kernel<BS, 3, 2>); \
-        cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
-        if (e0 != cudaSuccess) return e0;                                                                  \
-        void *args[] = {const_cast<PSweepArgs *>(&a)};                                                     \
-        e0 = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), grid, block, args, smem, s); \
-        if (e0 != cudaSuccess) return e0;                                                                  \
-    }
-    BILUK_BS_DISPATCH(p.bs, PSWEEP_LAUNCH)
-#undef PSWEEP_LAUNCH
+    const void *fn = nullptr;
+    cudaError_t e = psweep_kernel_of(p, &fn);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    void *args[] = {const_cast<PSweepArgs *>(&a)};
+    e = cudaLaunchCooperativeKernel(fn, dim3(p.ps.P), dim3(psweep_threads(p)), args, smem, s);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm) {
     const size_t smem = psweep_smem_bytes(p);
-#define POCC(BS)                                                                                                  \
-    {                                                                                                             \
-        auto kern = p.ps.groups == 2 ? psweep_kernel<BS, 2, 2>                                                    \
-                                     : (p.ps.nprod == 1 ? psweep_kernel<BS, 3, 1> : psweep_kernel<BS, 3, 2>);        \
-        cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));      \
-        if (e0 != cudaSuccess) return e0;                                                                         \
-        e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, p.ps.groups * PS_NG + 32 * p.ps.nprod, \
-                                                           smem);                                                 \
-        if (e0 != cudaSuccess) return e0;                                                                         \
-    }
-    BILUK_BS_DISPATCH(p.bs, POCC)
-#undef POCC
-    return cudaSuccess;
+    const void *fn = nullptr;
+    cudaError_t e = psweep_kernel_of(p, &fn);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, psweep_threads(p), smem);
 }
 
 }  // namespace biluk

@@ -67,13 +67,28 @@ class DeviceOperator:
         stream = enter()
         self._ws, wsp = alloc_bytes(L.biluk_op_workspace_bytes(h))
         nat.check(L.biluk_op_bind(h, wsp, L.biluk_op_workspace_bytes(h), stream))
-        self._vals = to_device_f64(vals)
-        nat.check(L.biluk_op_set_values(h, self._vals.data_ptr(), stream))
+        self._vals = None
+        self.set_values(vals)
         self.spmv_bytes = 8 * bs * bs * int(rp[-1]) + 4 * int(rp[-1]) + 4 * (n + 1) + 16 * bs * n
 
     @property
     def handle(self):
         return self._h
+
+    def set_values(self, vals):
+        """(Re)load the block values (same pattern) -- host or device float64, column-major blocks."""
+        t = torch()
+        stream = enter()
+        if self._vals is None:   # an own copy (never alias the caller's tensor)
+            self._vals = to_device_f64(vals)
+            if isinstance(vals, t.Tensor) and self._vals.data_ptr() == vals.data_ptr():
+                self._vals = self._vals.clone()
+        else:
+            src = vals if isinstance(vals, t.Tensor) else t.from_numpy(np.ascontiguousarray(vals, np.float64))
+            if src.numel() != self._vals.numel():
+                raise ValueError("set_values: value count does not match the operator's pattern")
+            self._vals.copy_(src.reshape(-1))
+        nat.check(nat.lib().biluk_op_set_values(self._h, self._vals.data_ptr(), stream))
 
     def matvec(self, x, out=None):
         t = torch()
@@ -90,7 +105,14 @@ _op_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def operator_for(a) -> DeviceOperator:
-    """Cached device operator of a matrix object (containers are immutable by contract)."""
+    """Device operator of a matrix object for one call (spmv / gmres / bicgstab).
+
+    The pattern analysis and workspace are cached per matrix object; the VALUES
+    are re-read on every call, because the reference containers let callers
+    edit them in place (``.blocks`` is a writable view, reference
+    test_sparse.py:123) -- e.g. a Newton loop refreshing its Jacobian.  Pass a
+    ``DeviceOperator`` to keep the values resident across calls.
+    """
     if isinstance(a, DeviceOperator):
         return a
     try:
@@ -103,4 +125,7 @@ def operator_for(a) -> DeviceOperator:
             _op_cache[a] = op
         except TypeError:
             pass
+    else:
+        from .sparse import as_bsr
+        op.set_values(as_bsr(a)[5])
     return op

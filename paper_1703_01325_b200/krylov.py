@@ -74,6 +74,7 @@ def _precond_args(M, length):
     if not callable(M):
         raise TypeError("M must be None, BlockIlukFactors or a callable")
     t = torch()
+    caught = []   # an exception raised by M, re-raised once the C call has returned
 
     def _cb(user, din, dout, stream):
         try:
@@ -81,13 +82,15 @@ def _precond_args(M, length):
             v = t.as_tensor(src, device="cuda").cpu().numpy()
             res = np.asarray(M(v), dtype=np.float64)
             if res.shape != (length,):
+                caught.append(ValueError(f"preconditioner returned shape {res.shape}, expected ({length},)"))
                 return nat.EARG
             t.as_tensor(_DevView(dout, length), device="cuda").copy_(t.from_numpy(res))
             return nat.OK
-        except Exception:   # the C side reports a failing callback
+        except Exception as exc:   # the C side stops the solve; the exception is re-raised in Python
+            caught.append(exc)
             return nat.ECUDA
     fn = nat.PRECOND_FN(_cb)
-    return None, fn, fn
+    return None, fn, (fn, caught)
 
 
 class _DevView:
@@ -129,6 +132,8 @@ def _solve(kind, a, b, M, cfg, restart):
     else:
         rc = L.biluk_bicgstab(op.handle, plan, cb, None, bd.data_ptr(), x.data_ptr(), workp, int(cfg.max_iters),
                               float(cfg.rel_tol), stats, hist_p, cap, stream)
+    if keep is not None and keep[1]:
+        raise keep[1][0]
     del keep
     nat.check(rc, stage=kind)
     st = SolveStats()
@@ -220,6 +225,8 @@ def bicgstab_batched(a, b, segments=None, M=None, cfg=None):
     stats = (ctypes.c_double * (4 * nsys))()
     rc = L.biluk_bicgstab_batched(op.handle, plan, cb, None, nsys, seg.ctypes.data_as(nat.P_i64), bd.data_ptr(),
                                   x.data_ptr(), workp, int(cfg.max_iters), float(cfg.rel_tol), stats, stream)
+    if keep is not None and keep[1]:
+        raise keep[1][0]
     del keep
     nat.check(rc, stage="bicgstab_batched")
     out = x if on_device else x.cpu().numpy()

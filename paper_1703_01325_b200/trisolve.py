@@ -92,6 +92,22 @@ def build_level_schedule(t):
     return LevelSchedule(lev, groups, nlev, t.orientation, t)
 
 
+def _check_out(out, length, bd):
+    """``out`` must be a contiguous float64 CUDA vector of the right length on
+    the current device, not overlapping the right-hand side."""
+    t = torch()
+    if not (isinstance(out, t.Tensor) and out.is_cuda):
+        raise ValueError("out must be a CUDA tensor")
+    if out.dtype != t.float64 or not out.is_contiguous() or out.numel() != length:
+        raise ValueError(f"out must be a contiguous float64 vector of length {length}")
+    if out.device.index != t.cuda.current_device():
+        raise ValueError("out is on another device")
+    lo, hi = out.data_ptr(), out.data_ptr() + 8 * length
+    blo, bhi = bd.data_ptr(), bd.data_ptr() + 8 * length
+    if lo < bhi and blo < hi:
+        raise ValueError("output may not overlap the right-hand side")
+
+
 def apply_preconditioner(f, b, workers=1, out=None):
     """x = U'^-1 D^-1 L^-1 b on the GPU (reference trisolve.py:169-182).
 
@@ -112,9 +128,9 @@ def apply_preconditioner(f, b, workers=1, out=None):
             raise ValueError(f"right-hand side length {b.shape} does not match {length}")
     stream = enter()
     bd = to_device_f64(b)
+    if out is not None:
+        _check_out(out, length, bd)
     x = out if out is not None else t.empty(length, dtype=t.float64, device="cuda")
-    if x.data_ptr() == bd.data_ptr():
-        raise ValueError("output may not alias the right-hand side")
     nat.check(nat.lib().biluk_plan_apply(f.handle, bd.data_ptr(), x.data_ptr(), stream), stage="apply")
     if on_device:
         return x

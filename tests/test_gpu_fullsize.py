@@ -1,14 +1,19 @@
-"""Full-size parity (BASELINE configs[1..3]) against the C restatement of the
-reference (oracle/coracle.c), plus size-independent properties at 128^3 ILU(2).
+"""Full-size parity (BASELINE configs[1..4]) against the C restatement of the
+reference (oracle/coracle.c), and size-independent properties at 128^3 ILU(2).
 
 Bars: factors and preconditioned vectors <= 1e-12 relative (max-norm), point
-level sets exact, BiCGSTAB iteration counts within +-1.
+level sets exact, Krylov iteration counts within +-1 (BiCGSTAB and GMRES(30)
+counts at 128^3 / 100^3 come from tests/golden/fullsize_iters.json, made by
+tests/golden/make_fullsize_golden.py with the same oracle).
 """
+
+import json
+import os
 
 import numpy as np
 import pytest
 
-from conftest import rel_err
+from conftest import GOLDEN_DIR, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -19,23 +24,31 @@ def b2(cuda_ok):
     return mod
 
 
-@pytest.mark.parametrize("nx,k", [(64, 1), (128, 0)])
+@pytest.mark.parametrize("nx,k", [(64, 1), (128, 0), (128, 1), (128, 2)])
 def test_fullsize_factors_and_apply_vs_c_oracle(b2, nx, k):
+    """BASELINE configs[1] and [2] (ILU(0), ILU(1), ILU(2) of 128^3): the planner's
+    own kernel choice (128^3 ILU(2): one producer warp) against the C oracle."""
     from oracle import coracle
     n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, 3, seed=0)
     a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
     f = b2.build_preconditioner(a, k)
+    if nx == 128:
+        assert f.info["engine"] == 1
+        assert f.info["sweep_warps"] == 3 * 4 + (1 if k >= 2 else 2)
     cf = coracle.CFactors(n, bs, rp, ci, vals, k)
     assert np.array_equal(f.L.row_ptr, cf.L_rp) and np.array_equal(f.L.col_idx, cf.L_ci)
     assert np.array_equal(f.uprime.row_ptr, cf.U_rp) and np.array_equal(f.uprime.col_idx, cf.U_ci)
     assert rel_err(f.L.values, cf.L_vals) <= 1e-12
     assert rel_err(f.uprime.values, cf.U_vals) <= 1e-12
     assert rel_err(f.dinv, cf.dinv) <= 1e-12
-    rhs = np.random.default_rng(1).standard_normal(n * bs)
-    assert rel_err(b2.apply_preconditioner(f, rhs), cf.apply(rhs)) <= 1e-12
-    if nx <= 64:   # point schedules of the zero-dropped expansions: exact
-        assert np.array_equal(f.lower_schedule.level_of_row, cf.lo_level_of_row)
-        assert np.array_equal(f.upper_schedule.level_of_row, cf.up_level_of_row)
+    for seed in (1, 2):
+        rhs = np.random.default_rng(seed).standard_normal(n * bs)
+        err = rel_err(b2.apply_preconditioner(f, rhs), cf.apply(rhs))
+        print(f"{nx}^3 ILU({k}) apply rel err {err:.2e}")
+        assert err <= 1e-12
+    # point schedules of the zero-dropped expansions: exact
+    assert np.array_equal(f.lower_schedule.level_of_row, cf.lo_level_of_row)
+    assert np.array_equal(f.upper_schedule.level_of_row, cf.up_level_of_row)
 
 
 def test_bicgstab_64cube_ilu1_iterations_vs_oracle(b2):
@@ -54,6 +67,50 @@ def test_bicgstab_64cube_ilu1_iterations_vs_oracle(b2):
     assert abs(st.iterations - its) <= 1
     assert st.final_relative_residual <= 1e-6
     assert np.abs(x - 1.0).max() <= 1e-3
+
+
+FULL = json.load(open(os.path.join(GOLDEN_DIR, "fullsize_iters.json")))
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_fullsize_krylov_iterations_vs_oracle_golden(b2, name):
+    """configs[2] BiCGSTAB + ILU(0) at 128^3, configs[3] GMRES(30) + ILU(1) at
+    100^3 with 4x4 and 8x8 blocks: iteration counts within +-1 of the oracle's."""
+    g = FULL[name]
+    nx, bs, k = g["grid"], g["bs"], g["k"]
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, bs, seed=0)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    import torch
+    b = torch.from_numpy(b2.synthetic.ones_rhs(n, bs, rp, ci, vals)).cuda()
+    f = b2.build_preconditioner(a, k)
+    solve = b2.bicgstab if g["solver"] == "bicgstab" else b2.gmres
+    x, st = solve(a, b, M=f, cfg=b2.SolverConfig(restart=30, rel_tol=1e-6))
+    print(name, "gpu", st.iterations, "oracle", g["iterations"])
+    assert st.converged == g["converged"]
+    assert abs(st.iterations - g["iterations"]) <= 1
+    assert st.final_relative_residual <= 1e-6
+
+
+def test_batch_systems_vs_oracle(b2):
+    """BASELINE configs[4]: the 64-system batch (64^3 b3 ILU(1)) as the bench
+    builds it -- one block-diagonal operator -- applied once; systems 0, 21, 42
+    and 63 of the result against the C oracle of each system alone."""
+    import torch
+    from oracle import coracle
+    mats = []
+    for s in range(64):
+        n, bs, rp, ci, vals = b2.reservoir_block_grid(64, 64, 64, 3, seed=s)
+        mats.append(b2.BcsrMatrix(bs, n, n, rp, ci, vals))
+    big = b2.block_diagonal(mats)
+    f = b2.build_preconditioner(big, 1)
+    m = n * bs
+    rhs = np.random.default_rng(9).standard_normal(64 * m)
+    z = b2.apply_preconditioner(f, torch.from_numpy(rhs).cuda()).cpu().numpy()
+    f.status()
+    for s in (0, 21, 42, 63):
+        a = mats[s]
+        cf = coracle.CFactors(a.num_block_rows, bs, a.row_ptr, a.col_idx, a.values, 1)
+        assert rel_err(z[s * m:(s + 1) * m], cf.apply(rhs[s * m:(s + 1) * m])) <= 1e-12, s
 
 
 def test_ilu2_128cube_properties(b2):

@@ -143,6 +143,76 @@ def test_bad_lengths_and_callable_preconditioner(b2):
     assert s0.iterations > s2.iterations          # preconditioning helps
     with pytest.raises(ValueError):
         b2.gmres(a, np.zeros(n * bs + 1))
+    # a failing user M surfaces as its own exception, a wrong-length result as ValueError
+    class Boom(Exception):
+        pass
+
+    def bad(v):
+        raise Boom("user preconditioner failed")
+    with pytest.raises(Boom):
+        b2.gmres(a, b, M=bad)
+    with pytest.raises(Boom):
+        b2.bicgstab(a, b, M=bad)
+    with pytest.raises(ValueError, match="shape"):
+        b2.gmres(a, b, M=lambda v: v[:-1])
+
+
+def test_mutated_matrix_values_reach_the_solvers(b2):
+    """A host matrix edited in place (e.g. a refreshed Jacobian) is re-read by
+    spmv / gmres / bicgstab on every call (no identity-only caching)."""
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(6, 5, 4, 3, seed=8)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals.copy())
+    x = np.random.default_rng(0).standard_normal(n * bs)
+    y1 = b2.spmv(a, x)
+    a.values[:] *= 2.0
+    y2 = b2.spmv(a, x)
+    assert np.allclose(y2, 2.0 * y1, rtol=1e-14, atol=0)
+    b = b2.spmv(a, np.ones(n * bs))
+    f = b2.build_preconditioner(a, 0)
+    xs, st = b2.bicgstab(a, b, M=f)
+    assert st.converged and np.abs(xs - 1.0).max() <= 1e-4
+
+
+def test_out_argument_is_checked(b2):
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(5, 5, 5, 3, seed=2)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0)
+    rhs = torch.ones(n * bs, dtype=torch.float64, device="cuda")
+    for bad in (torch.empty(n * bs - 1, dtype=torch.float64, device="cuda"),
+                torch.empty(n * bs, dtype=torch.float32, device="cuda"),
+                torch.empty(n * bs, dtype=torch.float64),
+                torch.empty(2 * n * bs, dtype=torch.float64, device="cuda")[::2]):
+        with pytest.raises(ValueError):
+            b2.apply_preconditioner(f, rhs, out=bad)
+    big = torch.ones(2 * n * bs, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):   # overlapping the right-hand side
+        b2.apply_preconditioner(f, big[: n * bs], out=big[n * bs // 2: n * bs // 2 + n * bs])
+
+
+def test_applies_on_two_streams_are_serialised(b2):
+    """One plan applied from two torch streams back to back: the library orders
+    the second apply after the first (shared sweep workspace), results exact."""
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(24, 24, 24, 3, seed=3)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 1)
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, 1)
+    r1 = np.random.default_rng(1).standard_normal(n * bs)
+    r2 = np.random.default_rng(2).standard_normal(n * bs)
+    d1, d2 = torch.from_numpy(r1).cuda(), torch.from_numpy(r2).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(4):
+        with torch.cuda.stream(s1):
+            o1 = b2.apply_preconditioner(f, d1)
+        with torch.cuda.stream(s2):
+            o2 = b2.apply_preconditioner(f, d2)
+        outs.append((o1, o2))
+    torch.cuda.synchronize()
+    f.status()
+    w1, w2 = of.apply(r1), of.apply(r2)
+    for o1, o2 in outs:
+        assert rel_err(o1.cpu().numpy(), w1) <= TOL and rel_err(o2.cpu().numpy(), w2) <= TOL
 
 
 def test_gmres_known_answers(b2):
@@ -213,6 +283,54 @@ def test_both_engines_match_oracle_and_are_repeatable(b2, monkeypatch, engine, c
     for _ in range(3):
         assert torch.equal(b2.apply_preconditioner(f, rt), x1)
     f.status()
+
+
+@pytest.mark.parametrize("groups,nprod", [(3, 1), (2, 2), (2, 1), (3, 2)])
+@pytest.mark.parametrize("case", ["grid16_b3_k0", "grid12_b3_k2", "grid10_b4_k1", "rand300_b3_k1"])
+def test_partitioned_kernel_variants_match_oracle(b2, monkeypatch, groups, nprod, case):
+    """Every instantiation of the partitioned sweep (compute groups x producer
+    warps; the planner picks one producer only for large ILU(2)+) against the oracle."""
+    monkeypatch.setenv("BILUK_ENGINE", "1")
+    monkeypatch.setenv("BILUK_GROUPS", str(groups))
+    monkeypatch.setenv("BILUK_NPROD", str(nprod))
+    kind, bsk, kk = case.split("_")
+    bs, k = int(bsk[1:]), int(kk[1:])
+    if kind.startswith("grid"):
+        nx = int(kind[4:])
+        n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, nx, nx, bs, seed=6)
+    else:
+        n, bs, rp, ci, vals = _random_pattern_matrix(int(kind[4:]), bs, seed=6)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    f = b2.build_preconditioner(a, k)
+    assert f.info["engine"] == 1 and f.info["sweep_warps"] == groups * 4 + nprod
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, k)
+    for seed in (3, 4):
+        rhs = np.random.default_rng(seed).standard_normal(n * bs)
+        assert rel_err(b2.apply_preconditioner(f, rhs), of.apply(rhs)) <= TOL
+    f.status()
+
+
+def test_sweep_dependency_timeout_is_reported_not_hung(b2, monkeypatch):
+    """Fault injection: a record made to wait on a row published after it.  The
+    partitioned sweep must time out (bounded waits, the hand-over passed on) and
+    report BILUK_ETIMEOUT as CudaPathError -- not hang the GPU."""
+    import torch
+    monkeypatch.setenv("BILUK_ENGINE", "1")
+    monkeypatch.setenv("BILUK_FAULT_GPOS", "1")
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(12, 12, 12, 3, seed=1)
+    a = b2.BcsrMatrix(bs, n, n, rp, ci, vals)
+    f = b2.build_preconditioner(a, 0)
+    monkeypatch.delenv("BILUK_FAULT_GPOS")
+    rhs = torch.from_numpy(np.random.default_rng(3).standard_normal(n * bs)).cuda()
+    from paper_1703_01325_b200._native import CudaPathError
+    with pytest.raises(CudaPathError, match="timed out"):
+        b2.apply_preconditioner(f, rhs)
+        torch.cuda.synchronize()
+        f.status()
+    # the plan recovers: a fresh plan of the same matrix is exact again
+    g = b2.build_preconditioner(a, 0)
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, 0)
+    assert rel_err(b2.apply_preconditioner(g, rhs.cpu().numpy()), of.apply(rhs.cpu().numpy())) <= TOL
 
 
 @pytest.mark.parametrize("k", [0, 1])
