@@ -55,6 +55,29 @@ const char *biluk_version(void);
 int biluk_set_device(int32_t device);
 
 /* ------------------------------------------------------------------------
+ * Dense-block and scatter stages (device buffers, float64)
+ * ---------------------------------------------------------------------- */
+
+/* block_invert (factor.py:38-70), batched: n row-major bs x bs blocks
+ * (the reference's (n, bs, bs) layout) -> their inverses, LU with partial
+ * pivoting and the reference's singularity rules (all-zero block; |pivot| <
+ * 1e-13 max|B|).  BILUK_ESINGULAR with *err_idx = the first singular block.
+ * Synchronises the stream. */
+int biluk_block_invert(int32_t bs, int64_t n, const double *dev_in, double *dev_out, int64_t *err_idx,
+                       void *stream);
+
+/* apply_block_diagonal (trisolve.py:148-166): z_I = dinv[I] y_I, dinv row-major
+ * (n, bs, bs).  Asynchronous. */
+int biluk_block_diag_apply(int32_t bs, int64_t n, const double *dev_dinv, const double *dev_y, double *dev_z,
+                           void *stream);
+
+/* materialize (factor.py:83-121), value side: dst[map[s]] = src[s] for nsrc
+ * blocks of bs2 doubles (dst pre-zeroed by the caller; the slot map is
+ * integer host work).  Asynchronous. */
+int biluk_scatter_blocks(int32_t bs2, int64_t nsrc, const int64_t *dev_map, const double *dev_src, double *dev_dst,
+                         void *stream);
+
+/* ------------------------------------------------------------------------
  * Host-side symbolic helpers (integer, bit-exact with the reference)
  * ---------------------------------------------------------------------- */
 
@@ -88,6 +111,12 @@ int biluk_level_schedule(int64_t m, const int64_t *row_ptr, const int64_t *col_i
 int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                       int32_t k, biluk_plan_t **out, int64_t *err_row);
 void biluk_plan_destroy(biluk_plan_t *plan);
+/* The same with flags: BILUK_PLAN_FACTOR_ONLY skips the sweep planning (the
+ * plan then serves biluk_plan_factor_lu only -- the reference's
+ * block_ilu0_factorize / point_ilu0_factorize, factor.py:151-205). */
+#define BILUK_PLAN_FACTOR_ONLY 1
+int biluk_plan_create_ex(int32_t bs, int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t k,
+                         int32_t flags, biluk_plan_t **out, int64_t *err_row);
 
 /* Device workspace the plan needs (bytes, 256-byte aligned pointer expected). */
 uint64_t biluk_plan_workspace_bytes(const biluk_plan_t *plan);
@@ -102,6 +131,22 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
  * (bs > 1) or BILUK_EZEROPIVOT (bs == 1) with *err_row = the first failing
  * block row, as the reference would report it (factor.py:202-203, :144-145). */
 int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream, int64_t *err_row);
+
+/* block_ilu0_factorize / point_ilu0_factorize (factor.py:151-205): stages
+ * materialize + factorize only.  dev_out_vals receives the in-place factored
+ * L\U values on the plan's ILU(k) pattern (nnz(P') * bs * bs, column-major
+ * blocks; unit-lower multipliers strictly below the diagonal, U unscaled).
+ * Errors as biluk_plan_factor.  Synchronises the stream. */
+int biluk_plan_factor_lu(biluk_plan_t *plan, const double *dev_a_vals, double *dev_out_vals, void *stream,
+                         int64_t *err_row);
+
+/* split_ldu (factor.py:230-289) of an already factored matrix: dev_lu_vals
+ * holds L\U on the plan's pattern (plan created with k = 0 on that pattern);
+ * D_i^-1 = block_invert(U_ii) (BILUK_ESINGULAR, *err_row = i), U' = D^-1 U,
+ * then the sweep records -- the plan is ready for biluk_plan_apply.  With
+ * D = I and T as L or U' this is also solve_unit_triangular
+ * (trisolve.py:121-145).  Synchronises the stream. */
+int biluk_plan_load_factored(biluk_plan_t *plan, const double *dev_lu_vals, void *stream, int64_t *err_row);
 
 /* apply_preconditioner(f, b) -- trisolve.py:169-182 (Alg. 7):
  * x = U'^{-1} D^{-1} L^{-1} b, one persistent sync-free kernel for both

@@ -8,13 +8,15 @@ device buffers only.  There is no CPU fallback.
 """
 
 from .errors import FactorizationError, MatrixMarketError, SingularBlockError, StructuralError
-from .factor import BlockIlukFactors, build_preconditioner, symbolic_phase
+from .factor import (BlockIlukFactors, block_ilu0_factorize, block_invert, build_preconditioner, materialize,
+                     point_ilu0_factorize, split_ldu, symbolic_phase)
 from .krylov import SolverConfig, SolveStats, bicgstab, bicgstab_batched, gmres
 from .sparse import (BcsrMatrix, CsrMatrix, PatternMatrix, assemble_csr, bcsr_from_csr, block_diagonal,
                      csr_expand, csr_from_triplets, extract_point_pattern)
 from .matrix_market import read_matrix_market
-from .trisolve import (LevelSchedule, TriangularOperand, apply_preconditioner, apply_preconditioner_many,
-                       build_level_schedule, strict_triangle)
+from .symbolic import coupled_iluk_oracle
+from .trisolve import (LevelSchedule, TriangularOperand, apply_block_diagonal, apply_preconditioner,
+                       apply_preconditioner_many, build_level_schedule, solve_unit_triangular, strict_triangle)
 from .device import DeviceOperator
 from .synthetic import gen_poisson_3d, reservoir_block_grid
 
@@ -35,8 +37,10 @@ def spmv(a, x, workers=1):
 __all__ = [
     "BcsrMatrix", "BlockIlukFactors", "CsrMatrix", "DeviceOperator", "FactorizationError", "LevelSchedule",
     "MatrixMarketError", "PatternMatrix", "SingularBlockError", "SolveStats", "SolverConfig", "StructuralError",
-    "TriangularOperand", "apply_preconditioner", "apply_preconditioner_many", "assemble_csr", "bcsr_from_csr",
-    "bicgstab", "bicgstab_batched", "block_diagonal", "build_level_schedule", "build_preconditioner",
-    "csr_expand", "csr_from_triplets", "extract_point_pattern", "gen_poisson_3d", "gmres", "read_matrix_market",
-    "reservoir_block_grid", "spmv", "strict_triangle", "symbolic_phase", "__version__",
+    "TriangularOperand", "apply_block_diagonal", "apply_preconditioner", "apply_preconditioner_many",
+    "assemble_csr", "bcsr_from_csr", "bicgstab", "bicgstab_batched", "block_diagonal", "block_ilu0_factorize",
+    "block_invert", "build_level_schedule", "build_preconditioner", "coupled_iluk_oracle", "csr_expand",
+    "csr_from_triplets", "extract_point_pattern", "gen_poisson_3d", "gmres", "materialize",
+    "point_ilu0_factorize", "read_matrix_market", "reservoir_block_grid", "solve_unit_triangular", "split_ldu",
+    "spmv", "strict_triangle", "symbolic_phase", "__version__",
 ]

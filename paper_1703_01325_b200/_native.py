@@ -42,6 +42,12 @@ _SIGS = {
     "biluk_level_schedule": (ctypes.c_int, [c_i64, c_vp, c_vp, c_i32, c_vp, P_i64]),
     "biluk_plan_create": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_i32, ctypes.POINTER(c_vp), P_i64]),
     "biluk_plan_destroy": (None, [c_vp]),
+    "biluk_plan_create_ex": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_i32, c_i32, ctypes.POINTER(c_vp), P_i64]),
+    "biluk_plan_factor_lu": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, P_i64]),
+    "biluk_plan_load_factored": (ctypes.c_int, [c_vp, c_vp, c_vp, P_i64]),
+    "biluk_block_invert": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, P_i64, c_vp]),
+    "biluk_block_diag_apply": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "biluk_scatter_blocks": (ctypes.c_int, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "biluk_plan_workspace_bytes": (c_u64, [c_vp]),
     "biluk_plan_bind": (ctypes.c_int, [c_vp, c_vp, c_u64, c_vp]),
     "biluk_plan_factor": (ctypes.c_int, [c_vp, c_vp, c_vp, P_i64]),

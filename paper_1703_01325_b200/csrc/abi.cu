@@ -115,6 +115,11 @@ int biluk_level_schedule(int64_t m, const int64_t *row_ptr, const int64_t *col_i
 
 int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t k,
                       biluk_plan_t **out, int64_t *err_row) {
+    return biluk_plan_create_ex(bs, n, row_ptr, col_idx, k, 0, out, err_row);
+}
+
+int biluk_plan_create_ex(int32_t bs, int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int32_t k,
+                         int32_t flags, biluk_plan_t **out, int64_t *err_row) {
     if (!out) return fail(BILUK_EARG, "null output");
     *out = nullptr;
     auto *h = new (std::nothrow) biluk_plan;
@@ -123,6 +128,20 @@ int biluk_plan_create(int32_t bs, int64_t n, const int64_t *row_ptr, const int64
     if (rc != BILUK_OK) {
         delete h;
         return rc;
+    }
+    if (flags & BILUK_PLAN_FACTOR_ONLY) {   // materialize + factorize only: no sweep plan, no apply
+        int dev0 = 0, sms0 = 148, smem0 = 227 * 1024;
+        if (cudaGetDevice(&dev0) == cudaSuccess) {
+            cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+            cudaDeviceGetAttribute(&smem0, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+        } else {
+            cudaGetLastError();
+        }
+        h->p.engine = 0;
+        h->p.factor_only = true;
+        plan_layout(h->p, sms0, size_t(smem0));
+        *out = h;
+        return BILUK_OK;
     }
     int dev = 0, sms = 148, smem = 227 * 1024;
     if (cudaGetDevice(&dev) == cudaSuccess) {
@@ -198,8 +217,9 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     p.ws = static_cast<unsigned char *>(dev_workspace);
     // launch configuration check: the persistent sweep needs every CTA resident
-    int per_sm = 0;
-    if (p.engine == 1) {
+    int per_sm = 1;
+    if (p.factor_only) {
+    } else if (p.engine == 1) {
         CUDA_TRY(psweep_occupancy(p, &per_sm), "sweep occupancy");
     } else {
         CUDA_TRY(sweep_occupancy(p, &per_sm), "sweep occupancy");
@@ -245,6 +265,8 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     return BILUK_OK;
 }
 
+static int split_and_pack(Plan &p, cudaStream_t s);
+
 int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream, int64_t *err_row) {
     if (!plan || !plan->p.bound) return fail(BILUK_EARG, "plan is not bound to a workspace");
     Plan &p = plan->p;
@@ -268,6 +290,11 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
             return fail(BILUK_EZEROPIVOT, "zero pivot at row " + std::to_string(h.ferr_row));
         return fail(BILUK_ESINGULAR, "singular diagonal block at row " + std::to_string(h.ferr_row));
     }
+    if (p.factor_only) return fail(BILUK_EARG, "plan was created for factorization only (biluk_plan_factor_lu)");
+    return split_and_pack(p, s);
+}
+
+static int split_and_pack(Plan &p, cudaStream_t s) {
     CUDA_TRY(launch_split(p, s), "split");
     if (p.engine == 1) {
         CUDA_TRY(launch_ppack(p, s), "pack");
@@ -279,10 +306,65 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
     return BILUK_OK;
 }
 
+static void reset_fstatus(Plan &p, cudaStream_t s) {
+    DevStatus *st = dev_status(p);
+    int32_t z[2] = {0, 0};
+    long long big = (long long)INT64_MAX;
+    cudaMemcpyAsync(&st->status, z, sizeof(z), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(&st->ferr_row, &big, sizeof(big), cudaMemcpyHostToDevice, s);
+}
+
+static int read_fstatus(Plan &p, cudaStream_t s, int64_t *err_row) {
+    DevStatus h{};
+    CUDA_TRY(cudaMemcpyAsync(&h, dev_status(p), sizeof(h), cudaMemcpyDeviceToHost, s), "status read");
+    CUDA_TRY(cudaStreamSynchronize(s), "factorize sync");
+    if (h.fstatus != 0) {
+        if (err_row) *err_row = h.ferr_row;
+        if (h.fstatus == BILUK_EZEROPIVOT) return fail(BILUK_EZEROPIVOT, "zero pivot at row " + std::to_string(h.ferr_row));
+        return fail(BILUK_ESINGULAR, "singular diagonal block at row " + std::to_string(h.ferr_row));
+    }
+    return BILUK_OK;
+}
+
+int biluk_plan_factor_lu(biluk_plan_t *plan, const double *dev_a_vals, double *dev_out_vals, void *stream,
+                         int64_t *err_row) {
+    if (!plan || !plan->p.bound) return fail(BILUK_EARG, "plan is not bound to a workspace");
+    Plan &p = plan->p;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    reset_fstatus(p, s);
+    CUDA_TRY(launch_materialize(p, dev_a_vals, s), "materialize");
+    CUDA_TRY(launch_factor(p, s), "factorize");
+    const int rc = read_fstatus(p, s, err_row);
+    if (rc != BILUK_OK) return rc;
+    const size_t bytes = size_t(p.nnzP) * p.bs * p.bs * 8;
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(dev_out_vals, p.ws + p.off.pvals, bytes, cudaMemcpyDeviceToDevice, s), "copy");
+    CUDA_TRY(cudaStreamSynchronize(s), "factorize sync");
+    p.factored = false;
+    return BILUK_OK;
+}
+
+int biluk_plan_load_factored(biluk_plan_t *plan, const double *dev_lu_vals, void *stream, int64_t *err_row) {
+    if (!plan || !plan->p.bound) return fail(BILUK_EARG, "plan is not bound to a workspace");
+    Plan &p = plan->p;
+    if (p.factor_only) return fail(BILUK_EARG, "plan was created for factorization only");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    reset_fstatus(p, s);
+    const size_t bytes = size_t(p.nnzP) * p.bs * p.bs * 8;
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(p.ws + p.off.pvals, dev_lu_vals, bytes, cudaMemcpyDeviceToDevice, s), "load");
+    CUDA_TRY(launch_diag_invert(p, s), "split");
+    const int rc = read_fstatus(p, s, err_row);
+    if (rc != BILUK_OK) {
+        p.factored = false;
+        return rc;
+    }
+    return split_and_pack(p, s);
+}
+
 static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream);
 
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream) {
     if (!plan || !plan->p.factored) return fail(BILUK_EARG, "plan is not factored");
+    if (plan->p.factor_only) return fail(BILUK_EARG, "plan was created for factorization only");
     Plan &p = plan->p;
     if (p.n == 0) return BILUK_OK;
     if (dev_b == dev_x) return fail(BILUK_EARG, "output may not alias the right-hand side");

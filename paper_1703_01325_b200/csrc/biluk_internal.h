@@ -240,6 +240,7 @@ struct Plan {
     // bound device pointers
     unsigned char *ws = nullptr;
     bool bound = false, factored = false;
+    bool factor_only = false;        // created by biluk_plan_create_ex(BILUK_PLAN_FACTOR_ONLY): no sweep plan
 };
 
 // A block sparse operator for SpMV: sliced-ELL tiles of R consecutive block

@@ -202,5 +202,90 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     }
 }
 
+// ===========================================================================
+// small dense block inverse: LU with partial pivoting, the rules of
+// block_invert (factor.py:38-70): all-zero block singular, |pivot| <
+// 1e-13 * max|B| singular, first maximal pivot wins (np.argmax).
+// a: column-major input (a[c*BS + r]); inv: column-major output.
+// ===========================================================================
+template <int BS>
+__device__ __forceinline__ bool block_invert(const double *a, double *inv) {
+    double lu[BS][BS];
+    double amax = 0.0;
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            lu[r][c] = a[c * BS + r];
+            amax = fmax(amax, fabs(lu[r][c]));
+        }
+    if (amax == 0.0) return false;
+    if (BS == 1) {
+        inv[0] = 1.0 / lu[0][0];
+        return true;
+    }
+    int perm[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) perm[r] = r;
+#pragma unroll
+    for (int c = 0; c < BS; ++c) {
+        int p = c;
+        double best = fabs(lu[c][c]);
+#pragma unroll
+        for (int r = c + 1; r < BS; ++r)
+            if (fabs(lu[r][c]) > best) {
+                best = fabs(lu[r][c]);
+                p = r;
+            }
+        if (best < 1e-13 * amax) return false;
+        if (p != c) {
+#pragma unroll
+            for (int q = 0; q < BS; ++q) {
+                const double t = lu[c][q];
+                lu[c][q] = lu[p][q];
+                lu[p][q] = t;
+            }
+            const int t = perm[c];
+            perm[c] = perm[p];
+            perm[p] = t;
+        }
+#pragma unroll
+        for (int r = c + 1; r < BS; ++r) {
+            lu[r][c] /= lu[c][c];
+#pragma unroll
+            for (int q = c + 1; q < BS; ++q) lu[r][q] -= lu[r][c] * lu[c][q];
+        }
+    }
+    // X = U^-1 L^-1 P  (row r of P is e_{perm[r]})
+    double x[BS][BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) x[r][q] = (perm[r] == q) ? 1.0 : 0.0;
+#pragma unroll
+    for (int r = 1; r < BS; ++r)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int m = 0; m < r; ++m) s += lu[r][m] * x[m][q];
+            x[r][q] -= s;
+        }
+#pragma unroll
+    for (int r = BS - 1; r >= 0; --r)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int m = r + 1; m < BS; ++m) s += lu[r][m] * x[m][q];
+            x[r][q] = (x[r][q] - s) / lu[r][r];
+        }
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+        for (int q = 0; q < BS; ++q) inv[q * BS + r] = x[r][q];
+    return true;
+}
+
 }  // namespace dev
 }  // namespace biluk

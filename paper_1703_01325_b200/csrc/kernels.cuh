@@ -65,6 +65,7 @@ size_t psweep_smem_bytes(const Plan &p);
 cudaError_t launch_materialize(const Plan &p, const double *avals, cudaStream_t s);
 cudaError_t launch_factor(const Plan &p, cudaStream_t s);
 cudaError_t launch_split(const Plan &p, cudaStream_t s);
+cudaError_t launch_diag_invert(const Plan &p, cudaStream_t s);   // stages.cu: D^-1 of a loaded factored matrix
 cudaError_t launch_pack(const Plan &p, cudaStream_t s);
 cudaError_t launch_pack_ell(const Op &o, const double *avals, cudaStream_t s);
 cudaError_t launch_sweep(const Plan &p, const SweepArgs &a, cudaStream_t s);

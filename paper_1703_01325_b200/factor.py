@@ -25,10 +25,11 @@ import numpy as np
 
 from . import _native as nat
 from .device import alloc_bytes, enter, to_device_f64
-from .errors import FactorizationError, StructuralError
-from .sparse import BcsrMatrix, PatternMatrix, as_bsr, csr_expand
+from .errors import FactorizationError, SingularBlockError, StructuralError
+from .sparse import BcsrMatrix, CsrMatrix, PatternMatrix, as_bsr, csr_expand
 
-__all__ = ["BlockIlukFactors", "build_preconditioner", "symbolic_phase"]
+__all__ = ["BlockIlukFactors", "block_ilu0_factorize", "block_invert", "build_preconditioner", "materialize",
+           "point_ilu0_factorize", "split_ldu", "symbolic_phase"]
 
 _INFO_KEYS = ("n", "bs", "k", "nnzb_a", "nnzb_p", "nL", "nU", "levels_L", "levels_U", "tiles_L", "tiles_U",
               "rows_per_tile", "workspace_bytes", "apply_bytes", "spmv_bytes", "sweep_ctas", "sweep_warps",
@@ -200,6 +201,195 @@ class BlockIlukFactors:
 
     def __repr__(self):
         return f"BlockIlukFactors(n={self.n}, bs={self.bs}, k={self.k})"
+
+
+def _new_plan(bs, n, rp, ci, k, flags=0):
+    """(handle, workspace tensor, aligned pointer) of a bound plan; raises with the
+    C status mapped (the caller adds the stage text)."""
+    L = nat.lib()
+    h = ctypes.c_void_p()
+    err = ctypes.c_int64(-1)
+    rc = L.biluk_plan_create_ex(bs, n, nat.ptr(rp), nat.ptr(ci), int(k), int(flags), ctypes.byref(h),
+                                ctypes.byref(err))
+    if rc != nat.OK:
+        return rc, int(err.value), None
+    try:
+        stream = enter()
+        nbytes = L.biluk_plan_workspace_bytes(h)
+        ws, wsp = alloc_bytes(nbytes)
+        nat.check(L.biluk_plan_bind(h, wsp, nbytes, stream), stage="materialize")
+    except BaseException:
+        L.biluk_plan_destroy(h)
+        raise
+    return nat.OK, -1, (h, ws, wsp)
+
+
+def _diag_slots(n, rp, ci):
+    """Slot of each row's diagonal entry, or the first row without one (-1, i)."""
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    hit = np.flatnonzero(ci == rows)
+    has = np.zeros(n, bool)
+    has[rows[hit]] = True
+    if not has.all():
+        return None, int(np.flatnonzero(~has)[0])
+    slot = np.empty(n, np.int64)
+    slot[rows[hit]] = hit
+    return slot, -1
+
+
+def block_invert(b):
+    """Inverse of a small dense block by LU with partial pivoting (reference factor.py:38-70).
+
+    Runs on the GPU (``biluk_block_invert``); also accepts a stack ``(m, bs, bs)``
+    and then inverts every block.  Raises ``SingularBlockError`` when a pivot
+    falls below 1e-13 times the block's largest magnitude or the block is all
+    zero.  Block sizes 1..8.
+    """
+    from .device import torch
+    arr = np.asarray(b, dtype=np.float64)
+    if arr.ndim not in (2, 3) or arr.shape[-1] != arr.shape[-2]:
+        raise StructuralError("block_invert needs a square block")
+    bs = arr.shape[-1]
+    stack = arr.reshape(-1, bs, bs)
+    if stack.shape[0] == 0:
+        return arr.copy()
+    t = torch()
+    stream = enter()
+    din = t.from_numpy(np.ascontiguousarray(stack)).cuda()
+    dout = t.empty_like(din)
+    bad = ctypes.c_int64(-1)
+    rc = nat.lib().biluk_block_invert(bs, stack.shape[0], din.data_ptr(), dout.data_ptr(), ctypes.byref(bad), stream)
+    if rc == nat.ESINGULAR:
+        where = "" if arr.ndim == 2 else f" (block {bad.value})"
+        raise SingularBlockError(f"singular block: pivot below 1e-13 of the largest magnitude{where}")
+    nat.check(rc, stage="block_invert")
+    return dout.cpu().numpy().reshape(arr.shape)
+
+
+def materialize(a, pprime):
+    """Copy of ``a`` with pattern exactly ``pprime``, zeros at the added
+    positions (reference factor.py:83-121).
+
+    ``a`` is a BcsrMatrix (zero blocks backfilled) or a CsrMatrix; every
+    stored position of ``a`` must appear in ``pprime`` (StructuralError
+    otherwise).  The slot map is integer host work; the values are scattered on
+    the GPU (``biluk_scatter_blocks``).
+    """
+    from .device import torch
+    bs, n, m, rp, ci, vals = as_bsr(a)
+    if m != n:
+        raise StructuralError("materialize requires a square matrix")
+    if int(pprime.n) != n:
+        raise StructuralError(f"pattern dimension {pprime.n} does not match matrix dimension {n}")
+    prp, pci = pprime.to_csr_arrays() if hasattr(pprime, "to_csr_arrays") else \
+        PatternMatrix(pprime.n, pprime.rows).to_csr_arrays()
+    # slot of every stored (i, j) of a inside pprime: keys i*n + j are sorted in both
+    arow = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    pkey = np.repeat(np.arange(n, dtype=np.int64), np.diff(prp)) * max(n, 1) + pci
+    akey = arow * max(n, 1) + ci
+    pos = np.searchsorted(pkey, akey)
+    bad = (pos >= pkey.size) | (pkey[np.minimum(pos, max(pkey.size - 1, 0))] != akey) if akey.size else \
+        np.zeros(0, bool)
+    if bad.any():
+        t0 = int(np.flatnonzero(bad)[0])
+        raise StructuralError(f"pattern is missing stored position ({int(arow[t0])}, {int(ci[t0])})")
+    bs2 = bs * bs
+    out = np.zeros(int(prp[-1]) * bs2)
+    if akey.size:
+        t = torch()
+        stream = enter()
+        dsrc = to_device_f64(vals)
+        dmap = t.from_numpy(np.ascontiguousarray(pos, np.int64)).cuda()
+        ddst = t.zeros(out.size, dtype=t.float64, device="cuda")
+        nat.check(nat.lib().biluk_scatter_blocks(bs2, akey.size, dmap.data_ptr(), dsrc.data_ptr(), ddst.data_ptr(),
+                                                 stream), stage="materialize")
+        out = ddst.cpu().numpy()
+    if hasattr(a, "block_size"):
+        return BcsrMatrix(bs, n, n, prp, pci, out)
+    return CsrMatrix(n, n, prp, pci, out)
+
+
+def _ilu0_in_place(aprime, point):
+    """Stages materialize + factorize of an ILU(0) on aprime's own pattern, on the GPU."""
+    bs, n, m, rp, ci, vals = as_bsr(aprime)
+    if n != m:
+        raise StructuralError("factorization requires a square matrix")
+    slot, missing = _diag_slots(n, rp, ci)
+    if slot is None:
+        raise StructuralError(f"row {missing} has no diagonal entry" if point else
+                              f"block row {missing} has no diagonal block")
+    rc, erow, plan = _new_plan(bs, n, rp, ci, 0, flags=1)   # BILUK_PLAN_FACTOR_ONLY
+    nat.check(rc, stage="factorize", row=erow)
+    h, ws, wsp = plan
+    L = nat.lib()
+    try:
+        from .device import torch
+        t = torch()
+        stream = enter()
+        dvals = to_device_f64(vals)
+        dout = t.empty_like(dvals)
+        err = ctypes.c_int64(-1)
+        rc = L.biluk_plan_factor_lu(h, dvals.data_ptr(), dout.data_ptr(), stream, ctypes.byref(err))
+        if rc == nat.EZEROPIVOT:
+            raise FactorizationError(f"zero pivot at row {err.value}", row=int(err.value))
+        if rc == nat.ESINGULAR:
+            raise SingularBlockError(f"singular diagonal block at row {err.value}", row=int(err.value))
+        nat.check(rc, stage="factorize")
+        aprime.values[...] = dout.cpu().numpy().reshape(aprime.values.shape)
+    finally:
+        L.biluk_plan_destroy(h)
+    return aprime
+
+
+def point_ilu0_factorize(aprime):
+    """ILU(0) on the stored pattern of a CsrMatrix, overwriting its values in
+    place (reference factor.py:151-162): unit-lower multipliers strictly below
+    the diagonal, the upper factor with its diagonal on and above it.  Runs the
+    level-scheduled factorization kernel on the GPU; a pivot below 1e-300
+    raises ``FactorizationError`` with ``.row``."""
+    if aprime.num_rows != aprime.num_cols:
+        raise StructuralError("factorization requires a square matrix")
+    return _ilu0_in_place(aprime, point=True)
+
+
+def block_ilu0_factorize(aprime):
+    """Block ILU(0) on the stored block pattern of a BcsrMatrix, in place
+    (reference factor.py:165-205), on the GPU.  A_ip <- A_ip D_p^-1, then
+    A_ij -= A_ip A_pj over the stored slots; U stays unscaled.  Block size one
+    is the point kernel.  A singular diagonal block raises
+    ``SingularBlockError`` with ``.row``."""
+    if aprime.num_block_rows != aprime.num_block_cols:
+        raise StructuralError("factorization requires a square matrix")
+    return _ilu0_in_place(aprime, point=aprime.block_size == 1)
+
+
+def split_ldu(f):
+    """Split an in-place factored block matrix into BlockIlukFactors (reference
+    factor.py:230-289): L = the strictly lower blocks, D_i^-1 =
+    block_invert(U_ii), U'_ij = D_i^-1 U_ij.  The factors live on the GPU and
+    are ready for ``apply_preconditioner``."""
+    bs, n, m, rp, ci, vals = as_bsr(f)
+    if n != m:
+        raise StructuralError("split requires a square matrix")
+    slot, missing = _diag_slots(n, rp, ci)
+    if slot is None:
+        raise StructuralError(f"block row {missing} has no diagonal block")
+    rc, erow, plan = _new_plan(bs, n, rp, ci, 0)
+    nat.check(rc, stage="split", row=erow)
+    h, ws, wsp = plan
+    L = nat.lib()
+    try:
+        stream = enter()
+        dvals = to_device_f64(vals)
+        err = ctypes.c_int64(-1)
+        rc = L.biluk_plan_load_factored(h, dvals.data_ptr(), stream, ctypes.byref(err))
+        if rc == nat.ESINGULAR:
+            raise SingularBlockError(f"singular diagonal block at row {err.value}", row=int(err.value))
+        nat.check(rc, stage="split")
+    except BaseException:
+        L.biluk_plan_destroy(h)
+        raise
+    return BlockIlukFactors(h, ws, wsp, dvals, bs, n, 0)
 
 
 def build_preconditioner(a, k):

@@ -25,7 +25,7 @@ from .errors import StructuralError
 from .sparse import CsrMatrix
 
 __all__ = ["TriangularOperand", "LevelSchedule", "strict_triangle", "build_level_schedule", "apply_preconditioner",
-           "apply_preconditioner_many"]
+           "apply_preconditioner_many", "solve_unit_triangular", "apply_block_diagonal"]
 
 
 class TriangularOperand:
@@ -90,6 +90,96 @@ def build_level_schedule(t):
     counts = np.bincount(lev, minlength=nlev + 1)[1:]
     groups = np.split(by, np.cumsum(counts)[:-1]) if nlev else []
     return LevelSchedule(lev, groups, nlev, t.orientation, t)
+
+
+def _unit_triangular_plan(t):
+    """A GPU plan whose factored matrix is I + T: D = I and T as L (lower) or
+    U' (upper), so its apply is (I + T)^-1 -- the sweep kernels run the solve."""
+    from .factor import BlockIlukFactors, _new_plan
+    m = t.matrix
+    n = int(m.num_rows)
+    rp = np.asarray(m.row_ptr, np.int64)
+    ci = np.asarray(m.col_idx, np.int64)
+    vals = np.asarray(m.values, np.float64)
+    cnt = np.diff(rp)
+    nrp = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt + 1, out=nrp[1:])
+    # the diagonal goes after the row's entries (lower) or before them (upper)
+    dpos = nrp[1:] - 1 if t.orientation == "lower" else nrp[:-1]
+    nci = np.empty(int(nrp[-1]), np.int64)
+    nv = np.empty(int(nrp[-1]))
+    off = np.ones(int(nrp[-1]), bool)
+    off[dpos] = False
+    nci[dpos] = np.arange(n)
+    nv[dpos] = 1.0
+    nci[off] = ci
+    nv[off] = vals
+    rc, erow, plan = _new_plan(1, n, nrp, nci, 0)
+    nat.check(rc, stage="solve_unit_triangular", row=erow)
+    h, ws, wsp = plan
+    dv = to_device_f64(nv)
+    err = ctypes.c_int64(-1)
+    try:
+        nat.check(nat.lib().biluk_plan_load_factored(h, dv.data_ptr(), enter(), ctypes.byref(err)),
+                  stage="solve_unit_triangular")
+    except BaseException:
+        nat.lib().biluk_plan_destroy(h)
+        raise
+    return BlockIlukFactors(h, ws, wsp, dv, 1, n, 0)
+
+
+def solve_unit_triangular(t, schedule, b, workers=1):
+    """Solve (I + T) x = b, T strictly triangular (reference trisolve.py:121-145).
+
+    The unit diagonal means no divisions.  The schedule must have been built
+    from ``t`` (StructuralError otherwise); ``workers`` never changes a bit of
+    the result; ``b`` is left untouched.  Runs as the GPU sweep of a plan of
+    I + T, built on first use and kept with the schedule (like the
+    reference's packed levels, a snapshot of T's values).  numpy in -> numpy
+    out; a CUDA tensor in -> a CUDA tensor out.
+    """
+    if getattr(schedule, "_source", None) is not t:
+        raise StructuralError("schedule was not built from this operand")
+    tt = torch()
+    on_device = isinstance(b, tt.Tensor) and b.is_cuda
+    if on_device:
+        if b.numel() != t.n or b.dim() != 1:
+            raise ValueError(f"right-hand side length {tuple(b.shape)} does not match n={t.n}")
+    else:
+        b = np.asarray(b, dtype=np.float64)
+        if b.shape != (t.n,):
+            raise ValueError(f"right-hand side length {b.shape} does not match n={t.n}")
+    if t.n == 0:
+        return b.clone() if on_device else b.copy()
+    plan = getattr(schedule, "_b200_plan", None)
+    if plan is None:
+        plan = _unit_triangular_plan(t)
+        schedule._b200_plan = plan
+    return apply_preconditioner(plan, b)
+
+
+def apply_block_diagonal(dinv, y, workers=1):
+    """z with z_I = dinv[I] @ y_I for each block row I (reference trisolve.py:148-166).
+
+    ``dinv`` is an (n, bs, bs) row-major stack; one small dense multiply per
+    block row on the GPU (``biluk_block_diag_apply``).  numpy in -> numpy out.
+    """
+    t = torch()
+    on_device = isinstance(y, t.Tensor) and y.is_cuda
+    d = dinv if isinstance(dinv, t.Tensor) else np.asarray(dinv, dtype=np.float64)
+    if d.ndim != 3 or d.shape[1] != d.shape[2]:
+        raise ValueError("dinv must be an (n, bs, bs) stack")
+    n, bs = int(d.shape[0]), int(d.shape[1])
+    yv = y if on_device else np.asarray(y, dtype=np.float64)
+    if tuple(yv.shape) != (n * bs,):
+        raise ValueError(f"operand length {tuple(yv.shape)} does not match {n * bs}")
+    stream = enter()
+    dd = to_device_f64(d.reshape(-1) if isinstance(d, t.Tensor) else np.ascontiguousarray(d).reshape(-1))
+    yd = to_device_f64(yv)
+    z = t.empty(n * bs, dtype=t.float64, device="cuda")
+    nat.check(nat.lib().biluk_block_diag_apply(bs, n, dd.data_ptr(), yd.data_ptr(), z.data_ptr(), stream),
+              stage="apply_block_diagonal")
+    return z if on_device else z.cpu().numpy()
 
 
 def _check_out(out, length, bd):
