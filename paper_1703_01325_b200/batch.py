@@ -3,9 +3,10 @@
 A single system is never split (block-Jacobi or halo exchange would change
 the preconditioner).  With G ranks, rank g solves the contiguous shard
 [g*S/G, (g+1)*S/G) of the S systems -- no collective on the data path; one
-all_gather of the per-system statistics at the end, and the wall time is the
-max over ranks.  The solver itself is a plain function so the sharding and
-gathering logic is testable on CPU (gloo) without a GPU.
+all_gather of the per-system statistics at the end, and the elapsed time is
+the max over ranks.  ``run_sharded`` is the driver bench.py uses; the local
+solve is a callable, so the sharding / gathering / reduction logic runs (and
+is tested) on CPU with the gloo backend as well.
 """
 
 from __future__ import annotations
@@ -25,15 +26,10 @@ class SystemResult:
 
 
 def shard(num_systems: int, world: int, rank: int) -> range:
-    """Contiguous, balanced shard of system indices owned by ``rank``."""
+    """Contiguous, balanced shard of system indices owned by ``rank`` (any S, G)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     return range(rank * num_systems // world, (rank + 1) * num_systems // world)
-
-
-def run_shard(num_systems: int, world: int, rank: int, solve_one) -> list:
-    """Solve this rank's systems; ``solve_one(index) -> SystemResult``."""
-    return [solve_one(i) for i in shard(num_systems, world, rank)]
 
 
 def gather_results(local: list, dist=None) -> list:
@@ -46,31 +42,28 @@ def gather_results(local: list, dist=None) -> list:
     return sorted(out, key=lambda r: r.system)
 
 
-def device_solver(nx: int, bs: int, k: int, rel_tol: float = 1e-6, method: str = "bicgstab"):
-    """solve_one for the GPU: seeded synthetic system -> ILU(k) -> Krylov (b = A 1)."""
-    import time
-
+def max_over_ranks(values, dist=None, device=None):
+    """Element-wise max of a list of floats over ranks (one all_reduce)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(v) for v in values]
     import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
 
-    from . import BcsrMatrix, bicgstab, build_preconditioner, gmres, SolverConfig
-    from .synthetic import ones_rhs, reservoir_block_grid
 
-    rank = torch.distributed.get_rank() if torch.distributed.is_initialized() else 0
+def run_sharded(num_systems: int, solve_local, dist=None, device=None):
+    """Shard ``num_systems`` over the ranks of ``dist`` and solve this rank's share.
 
-    def solve_one(i: int) -> SystemResult:
-        n, b_, rp, ci, vals = reservoir_block_grid(nx, nx, nx, bs, seed=i)
-        a = BcsrMatrix(b_, n, n, rp, ci, vals)
-        rhs = torch.from_numpy(ones_rhs(n, b_, rp, ci, vals)).cuda()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        f = build_preconditioner(a, k)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        solver = bicgstab if method == "bicgstab" else gmres
-        cfg = SolverConfig(rel_tol=rel_tol, restart=30)
-        _, st = solver(a, rhs, M=f, cfg=cfg)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        return SystemResult(i, rank, st.iterations, st.converged, st.final_relative_residual, t1 - t0, t2 - t1)
-
-    return solve_one
+    ``solve_local(indices) -> (list[SystemResult], timings: dict[str, float])``
+    solves the given global system indices on this rank (the seeds follow the
+    global index, so the union over ranks is the same batch for any G).
+    Returns (every rank's results by system, timings max-reduced over ranks).
+    """
+    world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+    rank = dist.get_rank() if dist is not None and dist.is_initialized() else 0
+    mine = shard(num_systems, world, rank)
+    local, timings = solve_local(list(mine))
+    keys = sorted(timings)
+    red = max_over_ranks([timings[k] for k in keys], dist, device)
+    return gather_results(local, dist), dict(zip(keys, red))

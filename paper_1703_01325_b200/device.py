@@ -59,6 +59,7 @@ class DeviceOperator:
         from .sparse import as_bsr
         bs, n, m, rp, ci, vals = as_bsr(a)
         self.bs, self.n, self.ncols = bs, n, m
+        self.batch_segments = getattr(a, "batch_segments", None)   # block_diagonal batches stay batches
         L = nat.lib()
         h = ctypes.c_void_p()
         nat.check(L.biluk_op_create(bs, n, m, nat.ptr(rp), nat.ptr(ci), ctypes.byref(h)))
