@@ -281,15 +281,23 @@ __device__ __forceinline__ void wait_values(const double *__restrict__ base, con
     for (int e = 0; e < NE; ++e)
 #pragma unroll
         for (int q = 0; q < BS; ++q) xv[e][q] = 0.0;   // entries never polled contribute zero
+    // the LSB words of the entries (their values land in xv directly)
+    double lw[NE];
     while (pend) {
+        // issue every pending load, then look at them (one round trip per round)
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+            if (pend & (1u << e))
+                ld_tagged_split<BS>((e == NE - 1 ? last_base : base) + int64_t(pos[e]) * tag_stride(BS), xv[e], lw[e]);
         uint32_t still = 0;
 #pragma unroll
         for (int e = 0; e < NE; ++e)
             if (pend & (1u << e)) {
-                double w[BS + 1];
-                ld_tagged<BS>((e == NE - 1 ? last_base : base) + int64_t(pos[e]) * tag_stride(BS), w);
-                if (row_ready<BS>(w, par))
-                    untag_row<BS>(w, xv[e]);
+                uint32_t ok = tag_of(lw[e]) == par;
+#pragma unroll
+                for (int c = 0; c < BS; ++c) ok &= (tag_of(xv[e][c]) == par);
+                if (ok)
+                    untag_split<BS>(xv[e], lw[e]);
                 else
                     still |= 1u << e;
             }
@@ -412,9 +420,9 @@ template <int BS>
 __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepArgs a) {
     constexpr int R = rows_per_tile(BS);
     constexpr int BS2 = BS * BS;
-    constexpr int CH = BS <= 3 ? 12 : (BS <= 4 ? 8 : (BS <= 6 ? 6 : 4));
-    // register-staged slots per row: ~40 doubles of matrix values (none for bs > 5)
-    constexpr int CHR = BS > 4 ? 0 : (BS == 4 ? 1 : ((40 / BS2) < CH ? (40 / BS2) : CH));
+    constexpr int CH = BS <= 4 ? 8 : (BS <= 6 ? 6 : 4);
+    // register-staged slots per row: ~27 doubles of matrix values (none for bs > 4)
+    constexpr int CHR = BS > 4 ? 0 : (BS == 4 ? 1 : ((27 / BS2) < CH ? (27 / BS2) : CH));
     constexpr int CHS = BS <= 3 ? 4 : (BS <= 4 ? 2 : 1);   // narrow-tile poll width
     constexpr int CHS_R = CHR < CHS ? CHR : CHS;
     extern __shared__ __align__(128) unsigned char smem[];
