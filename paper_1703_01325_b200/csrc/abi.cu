@@ -360,27 +360,60 @@ int biluk_plan_load_factored(biluk_plan_t *plan, const double *dev_lu_vals, void
     return split_and_pack(p, s);
 }
 
-static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream);
+static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream,
+                        const int *skip);
 
 int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream) {
+    return biluk::plan_apply(plan, dev_b, dev_x, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+}  // extern "C"
+
+// the apply with an optional device skip word (*skip != 0: every kernel of the
+// apply returns at once -- Krylov iterations captured in a CUDA graph after
+// the solve stopped)
+int biluk::plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t st, const int *skip) {
     if (!plan || !plan->p.factored) return fail(BILUK_EARG, "plan is not factored");
     if (plan->p.factor_only) return fail(BILUK_EARG, "plan was created for factorization only");
     Plan &p = plan->p;
     if (p.n == 0) return BILUK_OK;
     if (dev_b == dev_x) return fail(BILUK_EARG, "output may not alias the right-hand side");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     // applies of one plan share its workspace (tagged vectors, epoch): order an
-    // apply on a new stream after the previous one
-    if (plan->last_ev && plan->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, plan->last_ev, 0), "apply");
-    int rc = apply_launch(plan, dev_b, dev_x, st);
+    // apply on a new stream after the previous one.  Inside a stream capture
+    // the graph orders them; the capturing code re-marks the plan afterwards
+    // (plan_mark), since an event recorded in a capture cannot be waited on
+    // outside it.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cap), "apply");
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    if (!capturing && plan->last_ev && plan->last_stream != st)
+        CUDA_TRY(cudaStreamWaitEvent(st, plan->last_ev, 0), "apply");
+    int rc = apply_launch(plan, dev_b, dev_x, st, skip);
     if (rc != BILUK_OK) return rc;
+    if (capturing) return BILUK_OK;
+    return plan_mark(plan, st);
+}
+
+// the plan's last apply was issued on `st` (outside any capture)
+int biluk::plan_mark(biluk_plan_t *plan, cudaStream_t st) {
     if (!plan->last_ev) CUDA_TRY(cudaEventCreateWithFlags(&plan->last_ev, cudaEventDisableTiming), "apply");
     CUDA_TRY(cudaEventRecord(plan->last_ev, st), "apply");
     plan->last_stream = st;
     return BILUK_OK;
 }
 
-static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream) {
+// make `st` the stream of the plan's next apply without capturing a wait:
+// called before a CUDA graph capture on st
+int biluk::plan_adopt_stream(biluk_plan_t *plan, cudaStream_t st) {
+    if (plan->last_ev && plan->last_stream != st) CUDA_TRY(cudaStreamWaitEvent(st, plan->last_ev, 0), "apply");
+    plan->last_stream = st;
+    return BILUK_OK;
+}
+
+extern "C" {
+
+static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream,
+                        const int *skip) {
     Plan &p = plan->p;
     if (p.engine == 1) {
         PSweepArgs a{};
@@ -392,7 +425,7 @@ static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, 
         a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
         a.out = dev_x;
         a.st = dev_status(p);
-        a.skip_flag = nullptr;
+        a.skip_flag = skip;
         a.timeout_ns = 2000000000ull;
         a.ring_mask = p.ps.ring - 1;
         a.data_bytes = uint32_t(p.ps.data_ring);
@@ -400,7 +433,7 @@ static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, 
         a.nrec_total = int64_t(p.ps.rec.size());
         a.b_perm = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
         a.y_u = reinterpret_cast<double *>(p.ws + p.off.ps_yu);
-        CUDA_TRY(launch_permute_b(p, dev_b, static_cast<cudaStream_t>(stream)), "apply");
+        CUDA_TRY(launch_permute_b(p, dev_b, static_cast<cudaStream_t>(stream), skip), "apply");
         if (plan->tev[0]) CUDA_TRY(cudaEventRecord(plan->tev[0], static_cast<cudaStream_t>(stream)), "apply");
         CUDA_TRY(launch_psweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
         if (plan->tev[1]) CUDA_TRY(cudaEventRecord(plan->tev[1], static_cast<cudaStream_t>(stream)), "apply");
@@ -419,7 +452,7 @@ static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, 
     a.npos = plan_npos(p);
     a.out = dev_x;
     a.st = dev_status(p);
-    a.skip_flag = nullptr;
+    a.skip_flag = skip;
     a.stages = p.sweep_stages;
     a.stage_bytes = int(p.stage_bytes);
     a.timeout_ns = 2000000000ull;

@@ -304,3 +304,12 @@ struct biluk_plan {
 struct biluk_op {
     biluk::Op o;
 };
+
+namespace biluk {
+// biluk_plan_apply with a device skip word (abi.cu; Krylov graphs)
+int plan_apply(biluk_plan *plan, const double *dev_b, double *dev_x, cudaStream_t st, const int *skip);
+// order the plan's next apply on `st` outside a stream capture
+int plan_adopt_stream(biluk_plan *plan, cudaStream_t st);
+// record that the plan's last apply was issued on `st` (after graph replays)
+int plan_mark(biluk_plan *plan, cudaStream_t st);
+}  // namespace biluk

@@ -57,7 +57,7 @@ struct PSweepArgs {
     double *y_u;                 // y in U'-position order (written by the L sweep, read by U' records)
 };
 cudaError_t launch_ppack(const Plan &p, cudaStream_t s);
-cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s);
+cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s, const int *skip = nullptr);
 cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s);
 cudaError_t psweep_occupancy(const Plan &p, int *blocks_per_sm);
 size_t psweep_smem_bytes(const Plan &p);

@@ -9,7 +9,11 @@
 // reads back only what its stopping tests need.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -123,7 +127,10 @@ enum { FIN_NONE = 0, FIN_ALPHA, FIN_OMEGA, FIN_BETA, FIN_DIV, FIN_GMRES_H,
 struct BFin {
     int *state;
     double tol;
-    int64_t it;
+    int *alive;      // systems not yet stopped; the last one to stop sets *dead
+    int *dead;       // every system stopped: the skip word of the apply and SpMV launches
+    double *hist;    // one system: its residual history (S_NH entries), or null
+    int64_t hcap;
 };
 
 __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double *partials, int nq, int d0, int d1, int d2,
@@ -143,6 +150,16 @@ __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double *par
     }
     if (threadIdx.x != 0) return;
     int *st = bf.state ? bf.state + sys : nullptr;
+    auto stop = [&]() {   // state -> 2 (stopped), once per system
+        if (*st == 2) return;
+        *st = 2;
+        if (bf.alive && atomicSub(bf.alive, 1) == 1) *bf.dead = 1;
+    };
+    auto record = [&](double v) {   // history entry S_NH, then S_NH += 1
+        const int64_t k = int64_t(scal[S_NH]);
+        if (bf.hist && k < bf.hcap) bf.hist[k] = v;
+        scal[S_NH] += 1.0;
+    };
     switch (op) {
         case FIN_ALPHA:   // alpha = rho / <r^, v>
             if (scal[S_RV] != 0.0) scal[S_ALPHA] = scal[S_RHO] / scal[S_RV];
@@ -161,43 +178,46 @@ __global__ void __launch_bounds__(RED_THREADS) finalize_kernel(const double *par
             scal[S_BN] = sqrt(bb);
             scal[S_RHO] = bb; scal[S_RHO_PREV] = 1.0; scal[S_ALPHA] = 1.0; scal[S_OMEGA] = 1.0; scal[S_BETA] = bb;
             scal[S_ITS] = 0.0; scal[S_NH] = 0.0; scal[S_LAST] = INFINITY;
-            *st = bb == 0.0 ? 2 : 0;
-            if (bb == 0.0) scal[S_LAST] = 0.0;
+            *st = 0;
+            if (bb == 0.0) {
+                scal[S_LAST] = 0.0;
+                stop();
+            }
             break;
         }
         case FIN_B_ALPHA:
             if (*st != 0) break;
-            if (scal[S_RV] == 0.0) { *st = 2; break; }   // breakdown before the iteration counts
+            if (scal[S_RV] == 0.0) { stop(); break; }   // breakdown before the iteration counts
             scal[S_ALPHA] = scal[S_RHO] / scal[S_RV];
-            scal[S_ITS] = double(bf.it);
+            scal[S_ITS] += 1.0;
             break;
         case FIN_B_HALF: {
             if (*st != 0) break;
             const double sn = sqrt(scal[S_SS]) / scal[S_BN];
             scal[S_LAST] = sn;
             if (sn <= bf.tol) {   // x += alpha p^, stop
-                scal[S_XA] = scal[S_ALPHA]; scal[S_XW] = 0.0; scal[S_NH] += 1.0; *st = 1;
+                scal[S_XA] = scal[S_ALPHA]; scal[S_XW] = 0.0; record(sn); *st = 1;
             }
             break;
         }
         case FIN_B_OMEGA:
             if (*st != 0) break;
             scal[S_XA] = scal[S_ALPHA];
-            if (scal[S_TT] == 0.0) { scal[S_XW] = 0.0; scal[S_NH] += 1.0; *st = 1; break; }
+            if (scal[S_TT] == 0.0) { scal[S_XW] = 0.0; record(scal[S_LAST]); *st = 1; break; }
             scal[S_OMEGA] = scal[S_TS] / scal[S_TT];
             scal[S_XW] = scal[S_OMEGA];
             break;
         case FIN_B_BETA: {
-            if (*st == 1) { *st = 2; break; }
+            if (*st == 1) { stop(); break; }
             if (*st != 0) break;
             const double rn = sqrt(scal[S_RR]) / scal[S_BN];
             scal[S_LAST] = rn;
-            scal[S_NH] += 1.0;
+            record(rn);
             const double om = scal[S_OMEGA];
             scal[S_BETA] = (scal[S_RHO_NEXT] / scal[S_RHO]) * (scal[S_ALPHA] / om);
             scal[S_RHO_PREV] = scal[S_RHO];
             scal[S_RHO] = scal[S_RHO_NEXT];
-            if (rn <= bf.tol || om == 0.0 || scal[S_RHO] == 0.0) *st = 2;
+            if (rn <= bf.tol || om == 0.0 || scal[S_RHO] == 0.0) stop();
             break;
         }
         case FIN_B_TRUE:   // S_GEN1 = ||b - A x||^2
@@ -249,7 +269,10 @@ struct Ctx {
     int smax = 0;
     int sstride = 0;
     double tol = 0.0;
-    int64_t it = 0;
+    int *alive = nullptr, *dead = nullptr;   // device liveness words (batched engine)
+    double *hist = nullptr;                  // device residual history (one system)
+    int64_t hcap = 0;
+    const int *skip = nullptr;               // skip word of the SpMV and apply launches
 
     void fused(const Fused &f) {
         if (err) return;
@@ -260,7 +283,7 @@ struct Ctx {
     void fin(int nq, int d0, int d1, int d2, int op) {
         if (err) return;
         finalize_kernel<<<nsys, RED_THREADS, 0, s>>>(partials, nq, d0, d1, d2, op, scal, nullptr, sstride,
-                                                     BFin{state, tol, it});
+                                                     BFin{state, tol, alive, dead, hist, hcap});
         err = cudaGetLastError();
     }
     void dot(const double *a, const double *b, int dst) {
@@ -275,7 +298,7 @@ struct Ctx {
     }
     void spmv(const double *x, double *y) {
         if (err) return;
-        err = launch_spmv(A->o, x, y, nullptr, s);
+        err = launch_spmv(A->o, x, y, skip, s);
     }
     int sms() const { return A->o.num_sms; }
     int apply(const double *b, double *x);
@@ -304,13 +327,14 @@ struct Ctx {
 using namespace biluk;
 
 extern "C" int biluk_plan_apply(biluk_plan_t *plan, const double *dev_b, double *dev_x, void *stream);
+extern "C" const char *biluk_last_error(void);
 
 // preconditioner: plan apply, else the user callback, else identity
 int biluk::Ctx::apply(const double *b, double *x) {
     if (err) return BILUK_ECUDA;
     int rc = BILUK_OK;
     if (M) {
-        rc = biluk_plan_apply(M, b, x, s);
+        rc = plan_apply(M, b, x, s, skip);
     } else if (cb) {
         rc = cb(user, b, x, s);
         if (rc != BILUK_OK) fail(rc, "preconditioner callback failed");
@@ -324,6 +348,12 @@ int biluk::Ctx::apply(const double *b, double *x) {
     }
     return rc;
 }
+
+namespace biluk {
+int bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user, int32_t nsys, const int64_t *seg,
+                    const double *dev_b, double *dev_x, void *dev_work, int64_t max_iters, double rel_tol,
+                    double *stats, double *history, int64_t hist_cap, cudaStream_t stream);
+}  // namespace biluk
 
 static int krylov_fail(Ctx &c, const char *what) {
     // the preconditioner already set the message: pass its status on (e.g.
@@ -356,7 +386,7 @@ int biluk_dot(const double *dev_a, const double *dev_b, int64_t len, double *res
     f.qb[0] = dev_b;
     fused_kernel<<<RED_BLOCKS, RED_THREADS, 0, s>>>(f, len, scal, partials, nullptr, Batch{nullptr, nullptr, 0, 0});
     finalize_kernel<<<1, RED_THREADS, 0, s>>>(partials, 1, 0, 0, 0, FIN_NONE, scal, nullptr, 0,
-                                              BFin{nullptr, 0.0, 0});
+                                              BFin{nullptr, 0.0, nullptr, nullptr, nullptr, 0});
     cudaError_t e = cudaMemcpyAsync(result, scal, 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(BILUK_ECUDA, std::string("dot: ") + cudaGetErrorString(e));
@@ -372,6 +402,11 @@ int biluk_bicgstab(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *us
     if (M && (!M->p.factored || M->p.n * M->p.bs != A->o.n * A->o.bs))   // vectors must match; blockings may differ
         return fail(BILUK_EARG, "preconditioner does not match the operator");
     if (max_iters < 1 || !(rel_tol > 0.0)) return fail(BILUK_EARG, "bad solver configuration");
+    if (!cb && !std::getenv("BILUK_KRYLOV_HOST")) {   // device-driven loop (CUDA graph), one system
+        const int64_t seg1[2] = {0, A->o.n};
+        return bicgstab_engine(A, M, cb, user, 1, seg1, dev_b, dev_x, dev_work, max_iters, rel_tol, stats, history,
+                               hist_cap, static_cast<cudaStream_t>(stream));
+    }
     const int64_t len = A->o.n * A->o.bs;
     const int32_t precond = (M || cb) ? 1 : 0;
     const uint64_t vec = ((8 * uint64_t(len) + 255) / 256) * 256;
@@ -536,6 +571,26 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     if (seg[0] != 0 || seg[nsys] != A->o.n) return fail(BILUK_EARG, "batch segments must cover [0, n)");
     for (int32_t i = 0; i < nsys; ++i)
         if (seg[i + 1] < seg[i]) return fail(BILUK_EARG, "batch segments must be non-decreasing");
+    return bicgstab_engine(A, M, cb, user, nsys, seg, dev_b, dev_x, dev_work, max_iters, rel_tol, stats, nullptr, 0,
+                           static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// Device-driven BiCGSTAB over nsys independent systems (nsys = 1: biluk_bicgstab).
+//
+// Every scalar, stopping test and iteration count lives on the device: the
+// epilogue kernels (FIN_B_*) run the tests of biluk_bicgstab's host loop per
+// system and freeze a system once it stops (state word); when the last system
+// stops, a `dead` word makes every later SpMV and preconditioner apply return
+// at once.  One iteration is captured ONCE in a CUDA graph (when the
+// preconditioner is a plan -- a Python callback cannot be captured) and
+// replayed; the host reads the state words of iteration i-1 while iteration i
+// runs, so the GPU never waits for it, and at most one replay past the stop
+// is issued (all of its kernels skip).
+int biluk::bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user, int32_t nsys,
+                           const int64_t *seg, const double *dev_b, double *dev_x, void *dev_work, int64_t max_iters,
+                           double rel_tol, double *stats, double *history, int64_t hist_cap, cudaStream_t stream) {
     const int64_t bs = A->o.bs;
     const int64_t len = A->o.n * bs;
     const int32_t precond = (M || cb) ? 1 : 0;
@@ -553,20 +608,52 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     double *scal = partials + int64_t(RED_BLOCKS) * MAXQ * nsys;
     int64_t *dseg = reinterpret_cast<int64_t *>(scal + int64_t(B_STRIDE) * nsys);
     int *dstate = reinterpret_cast<int *>(dseg + nsys + 1);
-    Ctx c{A, M, cb, user, static_cast<cudaStream_t>(stream), len, scal, partials, 0};
+    int *dlive = dstate + nsys;   // alive, dead
+    // the solve runs on a private non-blocking stream (capturable, unlike the
+    // legacy default stream), ordered after / before the caller's stream
+    cudaStream_t gs = nullptr;
+    cudaEvent_t order = nullptr;
+    if (cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&order, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(order, stream) ||
+        cudaStreamWaitEvent(gs, order, 0)) {
+        if (gs) cudaStreamDestroy(gs);
+        if (order) cudaEventDestroy(order);
+        return fail(BILUK_ECUDA, "bicgstab: stream setup failed");
+    }
+    struct Rejoin {   // the caller's stream waits for everything issued on gs
+        cudaStream_t caller, gs;
+        cudaEvent_t ev;
+        ~Rejoin() {
+            cudaEventRecord(ev, gs);
+            cudaStreamWaitEvent(caller, ev, 0);
+            cudaEventDestroy(ev);
+            cudaStreamDestroy(gs);
+        }
+    } rejoin{stream, gs, order};
+    Ctx c{A, M, cb, user, gs, len, scal, partials, 0};
     c.nsys = nsys;
     c.seg = dseg;
     c.state = dstate;
     c.sstride = B_STRIDE;
     c.tol = rel_tol;
+    c.alive = dlive;
+    c.dead = dlive + 1;
     std::vector<int64_t> hseg(nsys + 1);
     for (int32_t i = 0; i <= nsys; ++i) hseg[i] = seg[i] * bs;
     for (int32_t i = 0; i < nsys; ++i) {
         stats[4 * i + 0] = 0; stats[4 * i + 1] = 0; stats[4 * i + 2] = INFINITY; stats[4 * i + 3] = 0;
     }
-    c.err = cudaMemcpyAsync(dseg, hseg.data(), 8 * (nsys + 1), cudaMemcpyHostToDevice, c.s);
+    double *dhist = nullptr;
+    if (history && hist_cap > 0 && nsys == 1) {
+        c.err = cudaMallocAsync(reinterpret_cast<void **>(&dhist), 8 * size_t(hist_cap), c.s);
+        c.hist = dhist;
+        c.hcap = hist_cap;
+    }
+    const int init_live[2] = {nsys, 0};
+    if (!c.err) c.err = cudaMemcpyAsync(dseg, hseg.data(), 8 * (nsys + 1), cudaMemcpyHostToDevice, c.s);
     if (!c.err) c.err = cudaMemsetAsync(dstate, 0, 4 * nsys, c.s);   // the <b, b> pass below reads it
-    if (!c.err) c.err = cudaStreamSynchronize(c.s);                   // hseg lives on the host
+    if (!c.err) c.err = cudaMemcpyAsync(dlive, init_live, sizeof(init_live), cudaMemcpyHostToDevice, c.s);
+    if (!c.err) c.err = cudaStreamSynchronize(c.s);                   // hseg, init_live live on the host
     c.zero(dev_x);
     c.smax = 2;
     {
@@ -581,23 +668,13 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     c.zero(v);
     const double *M_p = precond ? ph : pv;
     const double *M_s = precond ? sh : sv;
-    std::vector<int> hstate(nsys);
-    auto all_stopped = [&]() {
-        if (c.err) return true;
-        c.err = cudaMemcpyAsync(hstate.data(), dstate, 4 * nsys, cudaMemcpyDeviceToHost, c.s);
-        if (!c.err) c.err = cudaStreamSynchronize(c.s);
-        if (c.err) return true;
-        for (int x : hstate)
-            if (x != 2) return false;
-        return true;
-    };
-    for (int64_t it = 1; it <= max_iters && !all_stopped(); ++it) {
-        c.it = it;
+    c.skip = c.dead;
+    auto iteration = [&]() -> int {
         c.smax = 0;
         Fused f{};   // p = r + beta (p - omega v)
         f.op = 2; f.u = pv; f.v = v; f.x = r; f.ic0 = S_BETA; f.ic1 = S_OMEGA; f.sgn0 = 1.0; f.nq = 0;
         c.fused(f);
-        if (precond && c.apply(pv, ph) != BILUK_OK) return krylov_fail(c, "bicgstab_batched");
+        if (precond && c.apply(pv, ph) != BILUK_OK) return BILUK_ECUDA;
         c.spmv(M_p, v);
         Fused fv{};   // <r^, v> -> alpha
         fv.op = 0; fv.ic0 = fv.ic1 = -1; fv.nq = 1; fv.qa[0] = rh; fv.qb[0] = v;
@@ -607,7 +684,7 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
         fs.op = 1; fs.u = sv; fs.x = r; fs.v = v; fs.ic0 = S_ALPHA; fs.ic1 = -1; fs.sgn0 = -1.0; fs.nq = 1;
         c.fused(fs);
         c.fin(1, S_SS, 0, 0, FIN_B_HALF);
-        if (precond && c.apply(sv, sh) != BILUK_OK) return krylov_fail(c, "bicgstab_batched");
+        if (precond && c.apply(sv, sh) != BILUK_OK) return BILUK_ECUDA;
         c.spmv(M_s, t);
         Fused fd{};   // <t, t>, <t, s> -> omega
         fd.op = 0; fd.ic0 = fd.ic1 = -1; fd.nq = 2; fd.qa[0] = t; fd.qb[0] = t; fd.qa[1] = t; fd.qb[1] = sv;
@@ -623,9 +700,72 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
         fr.qa[0] = nullptr; fr.qb[0] = nullptr; fr.qa[1] = rh; fr.qb[1] = nullptr;
         c.fused(fr);
         c.fin(2, S_RR, S_RHO_NEXT, 0, FIN_B_BETA);
+        return c.err ? BILUK_ECUDA : BILUK_OK;
+    };
+    // one iteration as a CUDA graph (plan or no preconditioner)
+    cudaGraphExec_t gexec = nullptr;
+    const int adopt = (!c.err && !cb && M) ? plan_adopt_stream(M, c.s) : BILUK_OK;
+    if (!c.err && !cb && adopt == BILUK_OK) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const int rc = iteration();
+            const cudaError_t cerr = c.err;
+            const cudaError_t ec = cudaStreamEndCapture(c.s, &g);
+            cudaError_t ei = cudaErrorUnknown;
+            if (rc == BILUK_OK && ec == cudaSuccess && g) ei = cudaGraphInstantiate(&gexec, g, 0);
+            if (ei != cudaSuccess) gexec = nullptr;
+            if (std::getenv("BILUK_KRYLOV_DEBUG"))
+                fprintf(stderr, "[bicgstab_engine] capture: iteration %d / %s, end %s, instantiate %s\n", rc,
+                        cudaGetErrorString(cerr), cudaGetErrorString(ec), cudaGetErrorString(ei));
+            if (g) cudaGraphDestroy(g);
+            if (!gexec) {   // not capturable here: run the iterations eagerly
+                cudaGetLastError();
+                c.err = cudaSuccess;
+                c.prc = BILUK_OK;
+            }
+        } else {
+            cudaGetLastError();
+        }
     }
-    if (c.err) return krylov_fail(c, "bicgstab_batched");
+    const bool dbg = std::getenv("BILUK_KRYLOV_DEBUG") != nullptr;   // diagnostics: graph use and loop time
+    auto now = []() { return std::chrono::steady_clock::now(); };
+    const auto t_cap = now();
+    // host loop: replay, and look at the states of the previous iteration
+    static thread_local int *hstate = nullptr;   // two pinned stop words, kept for later solves
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (!hstate && !c.err) c.err = cudaMallocHost(reinterpret_cast<void **>(&hstate), 2 * sizeof(int));
+    for (cudaEvent_t &e : ev)
+        if (!c.err) c.err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    int rc = BILUK_OK;
+    for (int64_t it = 1; it <= max_iters && !c.err; ++it) {
+        if (gexec) {
+            c.err = cudaGraphLaunch(gexec, c.s);
+        } else if ((rc = iteration()) != BILUK_OK) {
+            break;
+        }
+        if (!c.err) c.err = cudaMemcpyAsync(hstate + (it & 1), c.dead, sizeof(int), cudaMemcpyDeviceToHost, c.s);
+        if (!c.err) c.err = cudaEventRecord(ev[it & 1], c.s);
+        if (it >= 2 && !c.err) {   // iteration it-1 is done by now, or soon: its stop word
+            c.err = cudaEventSynchronize(ev[(it - 1) & 1]);
+            if (!c.err && hstate[(it - 1) & 1] != 0) break;
+        }
+    }
+    if (gexec) {
+        cudaGraphExecDestroy(gexec);
+        if (M && !c.err) plan_mark(M, c.s);   // later applies on other streams wait for the replays
+    }
+    if (!c.err) c.err = cudaStreamSynchronize(c.s);
+    if (dbg)
+        fprintf(stderr, "[bicgstab_engine] graph=%d loop %.3f ms\n", gexec != nullptr,
+                std::chrono::duration<double, std::milli>(now() - t_cap).count());
+    for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    if (c.err || rc != BILUK_OK) {
+        if (dhist) cudaFreeAsync(dhist, c.s);
+        return krylov_fail(c, nsys == 1 ? "bicgstab" : "bicgstab_batched");
+    }
     // true residuals ||b_s - A_s x_s|| / ||b_s||
+    c.skip = nullptr;
     c.spmv(dev_x, t);
     if (!c.err) {
         sub_kernel<<<c.sms() * 8, 256, 0, c.s>>>(t, dev_b, t, len);
@@ -641,7 +781,13 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     std::vector<double> hs(size_t(B_STRIDE) * nsys);
     if (!c.err) c.err = cudaMemcpyAsync(hs.data(), scal, 8 * hs.size(), cudaMemcpyDeviceToHost, c.s);
     if (!c.err) c.err = cudaStreamSynchronize(c.s);
-    if (c.err) return krylov_fail(c, "bicgstab_batched");
+    if (!c.err && dhist) {
+        const int64_t nh = std::min<int64_t>(int64_t(hs[S_NH]), hist_cap);
+        if (nh > 0) c.err = cudaMemcpyAsync(history, dhist, 8 * size_t(nh), cudaMemcpyDeviceToHost, c.s);
+        if (!c.err) c.err = cudaStreamSynchronize(c.s);
+    }
+    if (dhist) cudaFreeAsync(dhist, c.s);
+    if (c.err) return krylov_fail(c, nsys == 1 ? "bicgstab" : "bicgstab_batched");
     for (int32_t i = 0; i < nsys; ++i) {
         const double *q = hs.data() + size_t(B_STRIDE) * i;
         stats[4 * i + 0] = q[S_ITS];
@@ -649,8 +795,10 @@ int biluk_bicgstab_batched(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
         stats[4 * i + 2] = q[S_TRUE];
         stats[4 * i + 3] = q[S_NH];
     }
-    return M ? biluk_plan_status(M, stream) : BILUK_OK;
+    return M ? biluk_plan_status(M, c.s) : BILUK_OK;
 }
+
+extern "C" {
 
 // GMRES(m), left preconditioned, MGS Arnoldi, Givens on the host (gmres.py:76-186)
 int biluk_gmres(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, void *user, const double *dev_b,

@@ -566,7 +566,8 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
 // b in L-position order (the L records' input bulk copies read it)
 template <int BS>
 __global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ lrow, const double *__restrict__ b,
-                                 double *__restrict__ bp) {
+                                 double *__restrict__ bp, const int *skip) {
+    if (skip && ld_relaxed_s32(skip) != 0) return;
     // a gather: position p takes b's row lrow[p]; the writes (the costlier
     // side of a permutation) are coalesced
     constexpr int VS = ps_vec_stride(BS);
@@ -664,13 +665,13 @@ cudaError_t launch_ppack(const Plan &p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s) {
+cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s, const int *skip) {
     const int32_t *posl = reinterpret_cast<const int32_t *>(p.ws + p.off.ps_posl);
     double *bp = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
     int64_t grid = (p.n + 255) / 256;
     if (grid > int64_t(p.num_sms) * 16) grid = int64_t(p.num_sms) * 16;
     if (grid < 1) grid = 1;
-#define PERM_LAUNCH(BS) permute_b_kernel<BS><<<unsigned(grid), 256, 0, s>>>(p.n, posl, b, bp);
+#define PERM_LAUNCH(BS) permute_b_kernel<BS><<<unsigned(grid), 256, 0, s>>>(p.n, posl, b, bp, skip);
     BILUK_BS_DISPATCH(p.bs, PERM_LAUNCH)
 #undef PERM_LAUNCH
     return cudaGetLastError();

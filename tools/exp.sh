@@ -1,1 +1,1 @@
-timeout 1700 python -m pytest tests -m gpu -q -x --durations=15 2>&1 | tail -30
+timeout 1700 python -m pytest tests -m gpu -q -x 2>&1 | tail -4
