@@ -33,8 +33,8 @@ def build(force=False, verbose=False):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC,-O3", "-diag-suppress", "128", "-shared", "-o", OUT + ".tmp"]
-    cmd += [os.path.join(HERE, s) for s in SOURCES] + ["-cudart", "static"]
+           "-Xcompiler", "-fPIC,-O3,-pthread", "-diag-suppress", "128", "-shared", "-o", OUT + ".tmp"]
+    cmd += [os.path.join(HERE, s) for s in SOURCES] + ["-cudart", "static", "-lpthread"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=HERE)

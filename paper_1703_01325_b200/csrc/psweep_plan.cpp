@@ -8,11 +8,13 @@
 // CTA per part, and the records a CTA streams are laid out back to back.
 // Integer work only; the values are packed on the device (ppack_kernel).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 
 #include "biluk_internal.h"
 
@@ -119,6 +121,187 @@ void partition_finish(Partition &pt) {
 void part_order(const std::vector<int32_t> &lev, const std::vector<int32_t> &rows, std::vector<int32_t> &ord) {
     ord = rows;
     std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return lev[a] < lev[b]; });
+}
+
+// run f(c) for c in [0, P) on the host's cores (the parts are independent)
+template <class F>
+void parallel_parts(int P, F f) {
+    unsigned nt = std::thread::hardware_concurrency();
+    if (const char *e = std::getenv("BILUK_PLAN_THREADS")) nt = unsigned(std::max(1, std::atoi(e)));
+    nt = std::max(1u, std::min<unsigned>(nt, unsigned(P)));
+    if (nt <= 1) {
+        for (int c = 0; c < P; ++c) f(c);
+        return;
+    }
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t)
+        pool.emplace_back([&]() {
+            for (int c = next++; c < P; c = next++) f(c);
+        });
+    for (std::thread &t : pool) t.join();
+}
+
+// the records of part c (both sweeps): the level-ordered rows cut into
+// chunks of <= nthreads rows of one level under the footprint caps; offsets
+// (record bytes, index words, value-map entries) relative to the part
+struct PartRecords {
+    std::vector<PRecInfo> rec;
+    std::vector<int32_t> idx, vmap;
+    int64_t rec_total = 0, max_rec = 0, max_glob = 0, nglob_total = 0;
+    int32_t nl = 0;   // L records
+    int rc = BILUK_OK;
+    std::string msg;
+};
+
+void build_part_records(const Plan &p, const Partition &pt, const std::vector<int32_t> &ordLc,
+                        const std::vector<int32_t> &ordUc, int c, PartRecords &out) {
+    const PSweep &ps = p.ps;
+    const int bs = p.bs, bs2 = bs * bs, vs = ps_vec_stride(bs);
+    const int32_t mask = ps.ring - 1;
+    std::vector<int32_t> gl;     // a record's deduplicated dependency positions
+    std::vector<int32_t> nfar;   // per row of a level group: dependencies outside the ring
+    struct Chunk {
+        size_t a, e;           // rows ord[a, e) of one level
+        int64_t lend;          // ring sequence number just past the level
+        int S;
+        int64_t far;           // dependencies outside the ring (upper bound, not deduplicated)
+    };
+    std::vector<Chunk> chunks;
+    {
+        const int32_t b0 = pt.base[c];
+        const int32_t m = pt.base[c + 1] - b0;
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool up = pass == 1;
+            const std::vector<int32_t> &ord = up ? ordUc : ordLc;
+            const std::vector<int32_t> &lev = up ? p.lev_U : p.lev_L;
+            const std::vector<int32_t> &pos = up ? ps.posU : ps.posL;
+            const int32_t seq_base = up ? m : 0;   // ring sequence continues from the L sweep
+            const size_t rec_begin = out.rec.size();
+            // a dependency j of a row of a level ending at sequence `lend` is on
+            // chip iff it is in this part and the level's own writes cannot have
+            // recycled its ring slot
+            auto in_ring = [&](int32_t j, int64_t lend) {
+                return pt.part_of[j] == c && seq_base + int64_t(pos[j] - b0) >= lend - ps.ring;
+            };
+            // ---- chunks: <= nthreads rows of one level under the caps
+            chunks.clear();
+            size_t g0 = 0;
+            while (g0 < ord.size()) {
+                size_t ge = g0;
+                while (ge < ord.size() && lev[ord[ge]] == lev[ord[g0]]) ++ge;
+                const int64_t lend = seq_base + int64_t(ge);
+                nfar.assign(ge - g0, 0);
+                for (size_t q = g0; q < ge; ++q) {
+                    const int32_t i = ord[q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int32_t s2 = fs; s2 < fs + ns; ++s2) nfar[q - g0] += in_ring(p.p_ci[s2], lend) ? 0 : 1;
+                }
+                size_t a = g0;
+                while (a < ge) {
+                    size_t e = a;
+                    int S = 0;
+                    int64_t far = 0;
+                    while (e < ge && int64_t(e - a) < ps.nthreads) {
+                        const int32_t i = ord[e];
+                        const int S2 = std::max<int>(S, nslot_of(p, i, up));
+                        const int64_t far2 = far + nfar[e - g0];
+                        const int nr = int(e - a + 1);
+                        if (e > a && (rec_foot_bytes(bs2, vs, nr, S2, int(far2), up) > ps.rec_cap || far2 > ps.glob_cap))
+                            break;
+                        S = S2;
+                        far = far2;
+                        ++e;
+                    }
+                    chunks.push_back({a, e, lend, S, far});
+                    a = e;
+                }
+                g0 = ge;
+            }
+            // ---- records: one chunk each (pairing two whole levels per record
+            // was measured neutral to slower, DESIGN.md §3)
+            for (size_t ci0 = 0; ci0 < chunks.size();) {
+                const size_t a = chunks[ci0].a, e = chunks[ci0].e;
+                const int nr = int(e - a);
+                const int S = chunks[ci0].S;
+                auto lend_of = [&](size_t) { return chunks[ci0].lend; };
+                gl.clear();
+                for (size_t q = a; q < e; ++q) {
+                    const int32_t i = ord[q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int32_t s2 = fs; s2 < fs + ns; ++s2)
+                        if (!in_ring(p.p_ci[s2], lend_of(q))) gl.push_back(pos[p.p_ci[s2]]);
+                }
+                std::sort(gl.begin(), gl.end());
+                gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+                const int nglob = int(gl.size());
+                const int64_t foot = rec_foot_bytes(bs2, vs, nr, S, nglob, up);
+                if (nglob > ps.glob_cap || foot > ps.data_ring / 4 || foot >= (int64_t(1) << 31)) {   // half a producer's half ring
+                    out.rc = BILUK_EUNSUPPORTED;
+                    out.msg = "a block row is too long for the partitioned sweep";
+                    return;
+                }
+                const int32_t lvl = lev[ord[a]];
+                PRecInfo info{};
+                info.nrows = nr;
+                info.S = S;
+                info.level = lvl * 2 + (up ? 1 : 0);
+                info.nglob = nglob;
+                info.pos0 = int32_t(b0 + int32_t(a));
+                info.bytes = uint32_t(rec_total_bytes(bs2, nr, S, nglob, up));
+                info.foot = uint32_t(foot);
+                info.idx_words = uint32_t(rec_index_words(nr, S, nglob, up));
+                info.off = uint64_t(out.rec_total);
+                info.idx_off = uint64_t(out.idx.size());
+                info.vmap_off = int64_t(out.vmap.size());
+                out.rec_total += info.bytes;
+                out.max_rec = std::max<int64_t>(out.max_rec, foot);
+                out.max_glob = std::max<int64_t>(out.max_glob, nglob);
+                out.nglob_total += nglob;
+                PRecHdr h{};
+                h.nrows = nr;
+                h.S = S;
+                h.nglob = nglob;
+                h.flags = (up ? 1 : 0) | (nr << 1) | (lvl << 10);
+                h.seq0 = int32_t(seq_base + int32_t(a));
+                h.pos0 = int32_t(b0 + int32_t(a));
+                h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
+                h.in_off = int32_t(info.bytes);
+                const size_t base = out.idx.size();
+                out.idx.resize(base + size_t(a16(4 * int64_t(info.idx_words)) / 4), 0);   // 16-byte aligned sections
+                std::memcpy(out.idx.data() + base, &h, sizeof(h));
+                int32_t *w = out.idx.data() + base + sizeof(PRecHdr) / 4;
+                for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
+                w += nr;
+                int32_t *desc = w;
+                int32_t *gpos = w + int64_t(S) * nr;
+                for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
+                const size_t vbase = out.vmap.size();
+                out.vmap.resize(vbase + size_t(S) * nr, -1);
+                for (int q = 0; q < nr; ++q) {
+                    const int32_t i = ord[a + q];
+                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        int32_t d = ps.ring;   // zero slot
+                        if (s2 < ns) {
+                            const int32_t j = p.p_ci[fs + s2];
+                            if (in_ring(j, lend_of(a + q))) {
+                                d = int32_t((seq_base + int64_t(pos[j] - b0)) & mask);
+                            } else {
+                                const int64_t at = std::lower_bound(gl.begin(), gl.end(), pos[j]) - gl.begin();
+                                d = -int32_t(at) - 1;   // fetched dependency `at`
+                            }
+                            out.vmap[vbase + size_t(s2) * nr + q] = fs + s2;
+                        }
+                        desc[int64_t(s2) * nr + q] = d;
+                    }
+                }
+                out.rec.push_back(info);
+                ++ci0;
+            }
+            if (!up) out.nl = int32_t(out.rec.size() - rec_begin);
+        }
+    }
 }
 
 }  // namespace
@@ -305,13 +488,17 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     ps.posL.assign(n, -1);
     ps.posU.assign(n, -1);
     std::vector<std::vector<int32_t>> ordL(P), ordU(P);
-    for (int c = 0; c < P; ++c) {
+    parallel_parts(P, [&](int c) {
         part_order(p.lev_L, pt.rows[c], ordL[c]);
         part_order(p.lev_U, pt.rows[c], ordU[c]);
         for (size_t q = 0; q < ordL[c].size(); ++q) ps.posL[ordL[c][q]] = int32_t(pt.base[c] + q);
         for (size_t q = 0; q < ordU[c].size(); ++q) ps.posU[ordU[c][q]] = int32_t(pt.base[c] + q);
-    }
+    });
 
+    // the records of every part, built independently (threads), then
+    // concatenated: offsets inside a part are relative until the merge
+    std::vector<PartRecords> built(P);
+    parallel_parts(P, [&](int c) { build_part_records(p, pt, ordL[c], ordU[c], c, built[c]); });
     ps.rec.clear();
     ps.idx.clear();
     ps.vmap.clear();
@@ -319,150 +506,25 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     std::vector<int32_t> part_nl(P, 0);   // L records of each part
     ps.rec_total = ps.max_rec = ps.max_glob = ps.nglob_total = 0;
     ps.nlrec_max = 0;
-    const int32_t mask = ps.ring - 1;
-    std::vector<int32_t> gl;     // a record's deduplicated dependency positions
-    std::vector<int32_t> nfar;   // per row of a level group: dependencies outside the ring
-    struct Chunk {
-        size_t a, e;           // rows ord[a, e) of one level
-        int64_t lend;          // ring sequence number just past the level
-        int S;
-        int64_t far;           // dependencies outside the ring (upper bound, not deduplicated)
-    };
-    std::vector<Chunk> chunks;
     for (int c = 0; c < P; ++c) {
+        PartRecords &pr = built[c];
+        if (pr.rc != BILUK_OK) return fail(pr.rc, pr.msg);
         ps.part_rec[c] = int32_t(ps.rec.size());
-        const int32_t b0 = pt.base[c];
-        const int32_t m = pt.base[c + 1] - b0;
-        for (int pass = 0; pass < 2; ++pass) {
-            const bool up = pass == 1;
-            const std::vector<int32_t> &ord = up ? ordU[c] : ordL[c];
-            const std::vector<int32_t> &lev = up ? p.lev_U : p.lev_L;
-            const std::vector<int32_t> &pos = up ? ps.posU : ps.posL;
-            const int32_t seq_base = up ? m : 0;   // ring sequence continues from the L sweep
-            const size_t rec_begin = ps.rec.size();
-            // a dependency j of a row of a level ending at sequence `lend` is on
-            // chip iff it is in this part and the level's own writes cannot have
-            // recycled its ring slot
-            auto in_ring = [&](int32_t j, int64_t lend) {
-                return pt.part_of[j] == c && seq_base + int64_t(pos[j] - b0) >= lend - ps.ring;
-            };
-            // ---- chunks: <= nthreads rows of one level under the caps
-            chunks.clear();
-            size_t g0 = 0;
-            while (g0 < ord.size()) {
-                size_t ge = g0;
-                while (ge < ord.size() && lev[ord[ge]] == lev[ord[g0]]) ++ge;
-                const int64_t lend = seq_base + int64_t(ge);
-                nfar.assign(ge - g0, 0);
-                for (size_t q = g0; q < ge; ++q) {
-                    const int32_t i = ord[q];
-                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                    for (int32_t s2 = fs; s2 < fs + ns; ++s2) nfar[q - g0] += in_ring(p.p_ci[s2], lend) ? 0 : 1;
-                }
-                size_t a = g0;
-                while (a < ge) {
-                    size_t e = a;
-                    int S = 0;
-                    int64_t far = 0;
-                    while (e < ge && int64_t(e - a) < ps.nthreads) {
-                        const int32_t i = ord[e];
-                        const int S2 = std::max<int>(S, nslot_of(p, i, up));
-                        const int64_t far2 = far + nfar[e - g0];
-                        const int nr = int(e - a + 1);
-                        if (e > a && (rec_foot_bytes(bs2, vs, nr, S2, int(far2), up) > ps.rec_cap || far2 > ps.glob_cap))
-                            break;
-                        S = S2;
-                        far = far2;
-                        ++e;
-                    }
-                    chunks.push_back({a, e, lend, S, far});
-                    a = e;
-                }
-                g0 = ge;
-            }
-            // ---- records: one chunk each (pairing two whole levels per record
-            // was measured neutral to slower, DESIGN.md §3)
-            for (size_t ci0 = 0; ci0 < chunks.size();) {
-                const size_t a = chunks[ci0].a, e = chunks[ci0].e;
-                const int nr = int(e - a);
-                const int S = chunks[ci0].S;
-                auto lend_of = [&](size_t) { return chunks[ci0].lend; };
-                gl.clear();
-                for (size_t q = a; q < e; ++q) {
-                    const int32_t i = ord[q];
-                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                    for (int32_t s2 = fs; s2 < fs + ns; ++s2)
-                        if (!in_ring(p.p_ci[s2], lend_of(q))) gl.push_back(pos[p.p_ci[s2]]);
-                }
-                std::sort(gl.begin(), gl.end());
-                gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
-                const int nglob = int(gl.size());
-                const int64_t foot = rec_foot_bytes(bs2, vs, nr, S, nglob, up);
-                if (nglob > ps.glob_cap || foot > ps.data_ring / 4 || foot >= (int64_t(1) << 31))   // half a producer's half ring
-                    return fail(BILUK_EUNSUPPORTED, "a block row is too long for the partitioned sweep");
-                const int32_t lvl = lev[ord[a]];
-                PRecInfo info{};
-                info.nrows = nr;
-                info.S = S;
-                info.level = lvl * 2 + (up ? 1 : 0);
-                info.nglob = nglob;
-                info.pos0 = int32_t(b0 + int32_t(a));
-                info.bytes = uint32_t(rec_total_bytes(bs2, nr, S, nglob, up));
-                info.foot = uint32_t(foot);
-                info.idx_words = uint32_t(rec_index_words(nr, S, nglob, up));
-                info.off = uint64_t(ps.rec_total);
-                info.idx_off = uint64_t(ps.idx.size());
-                info.vmap_off = int64_t(ps.vmap.size());
-                ps.rec_total += info.bytes;
-                ps.max_rec = std::max<int64_t>(ps.max_rec, foot);
-                ps.max_glob = std::max<int64_t>(ps.max_glob, nglob);
-                ps.nglob_total += nglob;
-                PRecHdr h{};
-                h.nrows = nr;
-                h.S = S;
-                h.nglob = nglob;
-                h.flags = (up ? 1 : 0) | (nr << 1) | (lvl << 10);
-                h.seq0 = int32_t(seq_base + int32_t(a));
-                h.pos0 = int32_t(b0 + int32_t(a));
-                h.vals_off = int32_t(rec_vals_off(nr, S, nglob, up));
-                h.in_off = int32_t(info.bytes);
-                const size_t base = ps.idx.size();
-                ps.idx.resize(base + size_t(a16(4 * int64_t(info.idx_words)) / 4), 0);   // 16-byte aligned sections
-                std::memcpy(ps.idx.data() + base, &h, sizeof(h));
-                int32_t *w = ps.idx.data() + base + sizeof(PRecHdr) / 4;
-                for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
-                w += nr;
-                int32_t *desc = w;
-                int32_t *gpos = w + int64_t(S) * nr;
-                for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
-                const size_t vbase = ps.vmap.size();
-                ps.vmap.resize(vbase + size_t(S) * nr, -1);
-                for (int q = 0; q < nr; ++q) {
-                    const int32_t i = ord[a + q];
-                    const int32_t fs = first_slot_of(p, i, up), ns = nslot_of(p, i, up);
-                    for (int s2 = 0; s2 < S; ++s2) {
-                        int32_t d = ps.ring;   // zero slot
-                        if (s2 < ns) {
-                            const int32_t j = p.p_ci[fs + s2];
-                            if (in_ring(j, lend_of(a + q))) {
-                                d = int32_t((seq_base + int64_t(pos[j] - b0)) & mask);
-                            } else {
-                                const int64_t at = std::lower_bound(gl.begin(), gl.end(), pos[j]) - gl.begin();
-                                d = -int32_t(at) - 1;   // fetched dependency `at`
-                            }
-                            ps.vmap[vbase + size_t(s2) * nr + q] = fs + s2;
-                        }
-                        desc[int64_t(s2) * nr + q] = d;
-                    }
-                }
-                ps.rec.push_back(info);
-                ++ci0;
-            }
-            if (!up) {
-                ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, int32_t(ps.rec.size() - rec_begin));
-                part_nl[c] = int32_t(ps.rec.size() - rec_begin);
-            }
+        part_nl[c] = pr.nl;
+        ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, pr.nl);
+        for (PRecInfo info : pr.rec) {
+            info.off += uint64_t(ps.rec_total);
+            info.idx_off += uint64_t(ps.idx.size());
+            info.vmap_off += int64_t(ps.vmap.size());
+            ps.rec.push_back(info);
         }
+        ps.rec_total += pr.rec_total;
+        ps.max_rec = std::max(ps.max_rec, pr.max_rec);
+        ps.max_glob = std::max(ps.max_glob, pr.max_glob);
+        ps.nglob_total += pr.nglob_total;
+        ps.idx.insert(ps.idx.end(), pr.idx.begin(), pr.idx.end());
+        ps.vmap.insert(ps.vmap.end(), pr.vmap.begin(), pr.vmap.end());
+        pr = PartRecords();   // free as we go
     }
     ps.part_rec[P] = int32_t(ps.rec.size());
     ps.part_rec.insert(ps.part_rec.end(), part_nl.begin(), part_nl.end());   // then P L-record counts
