@@ -27,6 +27,7 @@ namespace biluk {
 constexpr int RED_BLOCKS = 512;
 constexpr int RED_THREADS = 256;
 constexpr int MAXQ = 3;
+constexpr int64_t HIST_CAP = 65536;   // device residual-history entries kept in a Krylov workspace
 
 
 // scalar slots in DevStatus::scal
@@ -371,7 +372,8 @@ uint64_t biluk_krylov_workspace_bytes(int64_t len_, int32_t restart) {
     const uint64_t len = uint64_t(len_);
     const uint64_t vec = ((8 * len + 255) / 256) * 256;
     const uint64_t nvec = 8 + (restart > 0 ? uint64_t(restart) + 1 : 0);
-    return nvec * vec + 8 * RED_BLOCKS * MAXQ + 8 * (64 + uint64_t(restart > 0 ? restart : 0) + 2) + 4096;
+    return nvec * vec + 8 * RED_BLOCKS * MAXQ + 8 * (64 + uint64_t(restart > 0 ? restart : 0) + 2) + 4096 +
+           8 * uint64_t(HIST_CAP);
 }
 
 int biluk_dot(const double *dev_a, const double *dev_b, int64_t len, double *result, void *dev_work, void *stream) {
@@ -547,7 +549,8 @@ uint64_t biluk_krylov_batched_workspace_bytes(int64_t len_, int32_t nsys) {
     const uint64_t len = uint64_t(len_);
     const uint64_t vec = ((8 * len + 255) / 256) * 256;
     const uint64_t ns = uint64_t(nsys);
-    return 8 * vec + 8 * RED_BLOCKS * MAXQ * ns + 8 * B_STRIDE * ns + 8 * (ns + 1) + 4 * ns + 4096;
+    return 8 * vec + 8 * RED_BLOCKS * MAXQ * ns + 8 * B_STRIDE * ns + 8 * (ns + 1) + 4 * ns + 4096 +
+           8 * uint64_t(HIST_CAP);
 }
 
 // Batched BiCGSTAB: nsys independent systems packed as one block-diagonal
@@ -610,26 +613,27 @@ int biluk::bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     int *dstate = reinterpret_cast<int *>(dseg + nsys + 1);
     int *dlive = dstate + nsys;   // alive, dead
     // the solve runs on a private non-blocking stream (capturable, unlike the
-    // legacy default stream), ordered after / before the caller's stream
-    cudaStream_t gs = nullptr;
-    cudaEvent_t order = nullptr;
-    if (cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&order, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(order, stream) ||
-        cudaStreamWaitEvent(gs, order, 0)) {
-        if (gs) cudaStreamDestroy(gs);
-        if (order) cudaEventDestroy(order);
+    // legacy default stream; one per host thread and device, kept), ordered
+    // after / before the caller's stream
+    static thread_local cudaStream_t streams[64] = {};
+    static thread_local cudaEvent_t events[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail(BILUK_ECUDA, "bicgstab: no device");
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
         return fail(BILUK_ECUDA, "bicgstab: stream setup failed");
-    }
+    if (!events[dev] && cudaEventCreateWithFlags(&events[dev], cudaEventDisableTiming) != cudaSuccess)
+        return fail(BILUK_ECUDA, "bicgstab: event setup failed");
+    cudaStream_t gs = streams[dev];
+    if (cudaEventRecord(events[dev], stream) != cudaSuccess || cudaStreamWaitEvent(gs, events[dev], 0) != cudaSuccess)
+        return fail(BILUK_ECUDA, "bicgstab: stream ordering failed");
     struct Rejoin {   // the caller's stream waits for everything issued on gs
         cudaStream_t caller, gs;
         cudaEvent_t ev;
         ~Rejoin() {
             cudaEventRecord(ev, gs);
             cudaStreamWaitEvent(caller, ev, 0);
-            cudaEventDestroy(ev);
-            cudaStreamDestroy(gs);
         }
-    } rejoin{stream, gs, order};
+    } rejoin{stream, gs, events[dev]};
     Ctx c{A, M, cb, user, gs, len, scal, partials, 0};
     c.nsys = nsys;
     c.seg = dseg;
@@ -643,11 +647,11 @@ int biluk::bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     for (int32_t i = 0; i < nsys; ++i) {
         stats[4 * i + 0] = 0; stats[4 * i + 1] = 0; stats[4 * i + 2] = INFINITY; stats[4 * i + 3] = 0;
     }
-    double *dhist = nullptr;
+    double *dhist = nullptr;   // the residual history lives at the end of the workspace
     if (history && hist_cap > 0 && nsys == 1) {
-        c.err = cudaMallocAsync(reinterpret_cast<void **>(&dhist), 8 * size_t(hist_cap), c.s);
+        dhist = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(dlive + 2) + 255) & ~uintptr_t(255));
         c.hist = dhist;
-        c.hcap = hist_cap;
+        c.hcap = std::min<int64_t>(hist_cap, HIST_CAP);
     }
     const int init_live[2] = {nsys, 0};
     if (!c.err) c.err = cudaMemcpyAsync(dseg, hseg.data(), 8 * (nsys + 1), cudaMemcpyHostToDevice, c.s);
@@ -761,7 +765,6 @@ int biluk::bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
     if (c.err || rc != BILUK_OK) {
-        if (dhist) cudaFreeAsync(dhist, c.s);
         return krylov_fail(c, nsys == 1 ? "bicgstab" : "bicgstab_batched");
     }
     // true residuals ||b_s - A_s x_s|| / ||b_s||
@@ -782,11 +785,10 @@ int biluk::bicgstab_engine(biluk_op_t *A, biluk_plan_t *M, biluk_precond_fn cb, 
     if (!c.err) c.err = cudaMemcpyAsync(hs.data(), scal, 8 * hs.size(), cudaMemcpyDeviceToHost, c.s);
     if (!c.err) c.err = cudaStreamSynchronize(c.s);
     if (!c.err && dhist) {
-        const int64_t nh = std::min<int64_t>(int64_t(hs[S_NH]), hist_cap);
+        const int64_t nh = std::min<int64_t>(int64_t(hs[S_NH]), c.hcap);
         if (nh > 0) c.err = cudaMemcpyAsync(history, dhist, 8 * size_t(nh), cudaMemcpyDeviceToHost, c.s);
         if (!c.err) c.err = cudaStreamSynchronize(c.s);
     }
-    if (dhist) cudaFreeAsync(dhist, c.s);
     if (c.err) return krylov_fail(c, nsys == 1 ? "bicgstab" : "bicgstab_batched");
     for (int32_t i = 0; i < nsys; ++i) {
         const double *q = hs.data() + size_t(B_STRIDE) * i;
