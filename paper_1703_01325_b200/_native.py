@@ -14,6 +14,8 @@ import threading
 from .errors import FactorizationError, SingularBlockError, StructuralError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbiluk.so")
+# A/B experiments (tools/exp.sh) load another build of the same library
+LIB_PATH = os.environ.get("BILUK_LIB_PATH", LIB_PATH)
 
 OK, ESTRUCT, ESINGULAR, EZEROPIVOT, ECUDA, ETIMEOUT, EARG, ENOMEM, EUNSUPPORTED = range(9)
 

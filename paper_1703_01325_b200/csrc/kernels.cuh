@@ -55,6 +55,7 @@ struct PSweepArgs {
     int64_t nrec_total;
     const double *b_perm;        // b in L-position order (pvs doubles per position; launch_permute_b)
     double *y_u;                 // y in U'-position order (written by the L sweep, read by U' records)
+    int nowait;                  // diagnostics: take every dependency's first load as is (wrong results)
 };
 cudaError_t launch_ppack(const Plan &p, cudaStream_t s);
 cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s, const int *skip = nullptr);

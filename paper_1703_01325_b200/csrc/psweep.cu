@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             unsigned long long *dbg =
                 (a.trace && gt == 0 && r0 + i < 16384) ? a.trace + size_t(a.nrec_total + r0 + i) * 8 : nullptr;
             if (dbg) dbg[0] = clock64();
+            if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 1] = globaltimer();
             const unsigned char *rec = dring + slot_off[s];
             const PRecHdr h = *reinterpret_cast<const PRecHdr *>(rec);
             const int nr = h.nrows, S = h.S, ng = h.nglob;
@@ -440,13 +441,14 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                 }
             }
             if (dbg) dbg[1] = clock64();
+            if (a.trace && gt == 0) a.trace[size_t(r0 + i) * 8 + 2] = globaltimer();
             {
                 auto fetch_dep = [&](int e, double (&dv)[BS + 1], bool loaded) {
                     const double *src = gvec + size_t(gpos[e]) * TVS;
                     if (!loaded) ld_tagged<BS>(src, dv);
                     uint64_t t0 = 0;
                     uint32_t spins = 0;
-                    while (!row_ready<BS>(dv, par)) {
+                    while (!a.nowait && !row_ready<BS>(dv, par)) {
                         if (ps_timed_out(t0, spins, a)) {
                             *reinterpret_cast<volatile int *>(&abort_flag) = 1;
                             break;

@@ -3,7 +3,7 @@
     python tools/trace_psweep.py --nx 128 --k 0 --out gpurun_out/ptrace_k0.npz
 
 Stamps per record (globaltimer ns, csrc/psweep.cu): 0 bulk copy issued,
-1 landed (seen by the poll warp), 3 dependencies ready (poll retired),
+1 landed (seen by the compute group), 2 staged, 3 dependencies ready,
 4 compute start (before the hand-over barrier), 5 compute end,
 6 (cta << 32 | smid), 7 flags.  The debug rows after the records hold, for the
 first 16384 records, clock64 stamps of the compute group's stages (thread 0):
