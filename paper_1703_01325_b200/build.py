@@ -9,7 +9,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = ["csrc/plan.cpp", "csrc/psweep_plan.cpp", "csrc/abi.cu", "csrc/kernels.cu", "csrc/psweep.cu", "csrc/krylov.cu",
-           "csrc/stages.cu"]
+           "csrc/stages.cu", "csrc/gsweep.cu"]
 HEADERS = ["csrc/biluk_internal.h", "csrc/device_util.cuh", "csrc/kernels.cuh", "../include/biluk.h"]
 OUT = os.path.join(HERE, "_lib", "libbiluk.so")
 

@@ -164,6 +164,16 @@ int biluk_plan_create_ex(int32_t bs, int64_t n, const int64_t *row_ptr, const in
     // planning, which would only be discarded, outright)
     P.engine = (bs <= 4 && n <= (int64_t(1) << 22)) ? 1 : 0;
     if (env) P.engine = std::atoi(env) == 0 ? 0 : 1;
+    // ILU(0) of a 7-point block grid: the grid sweep (engine 2) when it plans
+    const bool want_grid = env ? std::atoi(env) == 2 : false;
+    if (want_grid) {
+        rc = plan_gsweep(P, sms, size_t(smem));
+        if (rc == BILUK_OK) {
+            P.engine = 2;
+        } else {
+            P.gs = GSweep{};
+        }
+    }
     if (P.engine == 1) {
         rc = plan_psweep(P, sms, size_t(smem), 0);
         const double per_part = P.ps.P > 0 ? double(P.ps.rec.size()) / P.ps.P : 0.0;
@@ -219,6 +229,8 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
     // launch configuration check: the persistent sweep needs every CTA resident
     int per_sm = 1;
     if (p.factor_only) {
+    } else if (p.engine == 2) {
+        CUDA_TRY(gsweep_occupancy(p, &per_sm), "sweep occupancy");
     } else if (p.engine == 1) {
         CUDA_TRY(psweep_occupancy(p, &per_sm), "sweep occupancy");
     } else {
@@ -250,6 +262,12 @@ int biluk_plan_bind(biluk_plan_t *plan, void *dev_workspace, uint64_t bytes, voi
         CUDA_TRY(cudaMemcpyAsync(p.ws + p.off.ps_posl, lrow.data(), 4 * lrow.size(), cudaMemcpyHostToDevice, s),
                  "upload");
         CUDA_TRY(cudaStreamSynchronize(s), "upload sync");
+    }
+    if (p.engine == 2) {
+        CUDA_TRY(up(p.off.gs_part, p.gs.part.data(), sizeof(GPart) * p.gs.part.size()), "upload");
+        CUDA_TRY(up(p.off.gs_rec, p.gs.rec.data(), sizeof(GRec) * p.gs.rec.size()), "upload");
+        CUDA_TRY(up(p.off.gs_lo, p.gs.rec_lo.data(), 4 * p.gs.rec_lo.size()), "upload");
+        CUDA_TRY(up(p.off.gs_cols, p.gs.cols.data(), 4 * p.gs.cols.size()), "upload");
     }
     CUDA_TRY(up(p.off.pos_l, p.sl.pos.data(), 4 * p.sl.pos.size()), "upload");
     CUDA_TRY(up(p.off.pos_u, p.su.pos.data(), 4 * p.su.pos.size()), "upload");
@@ -296,7 +314,9 @@ int biluk_plan_factor(biluk_plan_t *plan, const double *dev_a_vals, void *stream
 
 static int split_and_pack(Plan &p, cudaStream_t s) {
     CUDA_TRY(launch_split(p, s), "split");
-    if (p.engine == 1) {
+    if (p.engine == 2) {
+        CUDA_TRY(launch_gpack(p, s), "pack");
+    } else if (p.engine == 1) {
         CUDA_TRY(launch_ppack(p, s), "pack");
     } else {
         CUDA_TRY(launch_pack(p, s), "pack");
@@ -415,6 +435,32 @@ extern "C" {
 static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, cudaStream_t stream,
                         const int *skip) {
     Plan &p = plan->p;
+    if (p.engine == 2) {
+        GSweepArgs a{};
+        a.parts = reinterpret_cast<const GPart *>(p.ws + p.off.gs_part);
+        a.recs = reinterpret_cast<const GRec *>(p.ws + p.off.gs_rec);
+        a.cols = reinterpret_cast<const int32_t *>(p.ws + p.off.gs_cols);
+        a.stream = p.ws + p.off.gs_stream;
+        a.b = dev_b;
+        a.y = reinterpret_cast<double *>(p.ws + p.off.gs_y);
+        a.out = dev_x;
+        a.y_t = reinterpret_cast<double *>(p.ws + p.off.y_t);
+        a.x_t = reinterpret_cast<double *>(p.ws + p.off.x_t);
+        a.st = dev_status(p);
+        a.skip_flag = skip;
+        a.timeout_ns = 2000000000ull;
+        a.nx = p.gs.nx;
+        a.ny = p.gs.ny;
+        a.nz = p.gs.nz;
+        a.slot_bytes = p.gs.slot_bytes;
+        a.kslots = p.gs.kslots;
+        a.trace = p.trace;
+        a.nrec_total = int64_t(p.gs.rec.size());
+        if (plan->tev[0]) CUDA_TRY(cudaEventRecord(plan->tev[0], static_cast<cudaStream_t>(stream)), "apply");
+        CUDA_TRY(launch_gsweep(p, a, static_cast<cudaStream_t>(stream)), "apply");
+        if (plan->tev[1]) CUDA_TRY(cudaEventRecord(plan->tev[1], static_cast<cudaStream_t>(stream)), "apply");
+        return BILUK_OK;
+    }
     if (p.engine == 1) {
         PSweepArgs a{};
         a.rec = reinterpret_cast<const PRecInfo *>(p.ws + p.off.ps_info);
@@ -560,13 +606,15 @@ int biluk_plan_status(biluk_plan_t *plan, void *stream) {
 int biluk_plan_info(const biluk_plan_t *plan, int64_t *info, int32_t ninfo) {
     if (!plan) return fail(BILUK_EARG, "null plan");
     const Plan &p = plan->p;
+    const bool g2 = p.engine == 2;
     const int64_t v[] = {p.n,          p.bs,         p.k,           p.nnzA,          p.nnzP,
                          p.nL,         p.nU,         p.nlev_L,      p.nlev_U,        p.sl.ntiles,
                          p.su.ntiles,  rows_per_tile(p.bs), int64_t(p.off.total), apply_bytes(p), spmv_bytes(p),
                          p.sweep_ctas, p.sweep_warps, p.sweep_stages, p.stage_bytes,
-                         std::max(p.sl.max_slots, p.su.max_slots), p.engine, p.ps.P,
-                         int64_t(p.ps.rec.size()), int64_t(p.ps.est_us * 1000.0), p.ps.rec_total,
-                         p.ps.nglob_total, p.ps.partition, p.ps.split[0], p.ps.split[1]};
+                         std::max(p.sl.max_slots, p.su.max_slots), p.engine, g2 ? p.gs.P : p.ps.P,
+                         g2 ? int64_t(p.gs.rec.size()) : int64_t(p.ps.rec.size()), int64_t(p.ps.est_us * 1000.0),
+                         g2 ? p.gs.stream_bytes : p.ps.rec_total, p.ps.nglob_total, g2 ? 1 : p.ps.partition,
+                         g2 ? p.gs.py : p.ps.split[0], g2 ? p.gs.pz : p.ps.split[1]};
     const int nv = int(sizeof(v) / sizeof(v[0]));
     for (int i = 0; i < ninfo; ++i) info[i] = i < nv ? v[i] : 0;
     return BILUK_OK;

@@ -207,6 +207,46 @@ struct PSweep {
     double est_us = 0;               // planner's time estimate for the chosen P
 };
 
+// ---------------------------------------------------------------------------
+// Grid sweep (engine 2; gsweep.cu): ILU(0) of a 7-point block
+// stencil on an nx x ny x nz natural-order grid.  The parts are the (y, z)
+// column blocks of the partitioned sweep (<= 128 columns each, one CTA per
+// part).  Thread t of a part owns column t (columns ordered by d = y + z, so
+// the columns holding a row of level s = x + d are a contiguous range) and
+// walks its column's rows level by level: the x-1 (U': x+1) dependency is the
+// thread's own previous result (a register), the y and z neighbours are the
+// neighbouring threads' previous results (shared memory, double-buffered,
+// one named barrier per level), or -- on a part face -- the rows other parts
+// publish to the parity-tagged vectors (polled ahead by halo warps).  The
+// factor blocks stream as one record per (part, level):
+//   hdr  int32[4]  nrows, lo (first column), stride R (rows, even), 0
+//   L:   f64[3][bs*bs][R]            blocks of the x-1, y-1, z-1 neighbours
+//   U':  f64[bs*bs][R] D^-1, then f64[3][bs*bs][R]  (x+1, y+1, z+1)
+// (zero blocks where a neighbour is outside the grid).
+// ---------------------------------------------------------------------------
+struct GPart {          // 32 bytes
+    int32_t y0, y1, z0, z1;
+    int32_t ncols;      // columns (<= 128), ordered by (y + z, y)
+    int32_t nl, nu;     // L and U' records
+    int32_t rec0;       // first record
+};
+struct GRec {           // 16 bytes
+    int64_t off;        // byte offset of the record in the stream
+    int32_t bytes;      // record bytes (multiple of 16)
+    int32_t nrows;
+};
+struct GSweep {
+    int32_t P = 0, py = 0, pz = 0;
+    int64_t nx = 0, ny = 0, nz = 0;
+    int32_t ne = 0;                  // halo entries of a part (max over parts and sweeps)
+    int32_t slot_bytes = 0, kslots = 0;
+    int64_t stream_bytes = 0;
+    std::vector<GPart> part;
+    std::vector<GRec> rec;
+    std::vector<int32_t> rec_lo;     // first column of each record
+    std::vector<int32_t> cols;       // P * 128: (y << 16) | z of each part's columns
+};
+
 struct Plan {
     int32_t bs = 0, k = 0;
     int64_t n = 0;
@@ -223,7 +263,8 @@ struct Plan {
     int32_t max_row_len = 0;         // longest P' row (factor shared memory)
     Sweep sl, su;                    // L sweep, U' sweep
     PSweep ps;                       // partitioned sweep layout
-    int32_t engine = 1;              // 1: partitioned sweep, 0: tiled level-order sweep
+    GSweep gs;                       // grid sweep layout
+    int32_t engine = 1;              // 2: grid sweep, 1: partitioned sweep, 0: tiled level-order sweep
     std::vector<uint32_t> lvl_tiles; // tiles per combined level (L levels, then U' levels), 1-based
     SweepTune tune;
     unsigned long long *trace = nullptr;   // optional per-tile timing records (diagnostics)
@@ -235,7 +276,7 @@ struct Plan {
     struct {
         uint64_t p_rp, p_ci, p_diag, a2p, forder, pvals, dinv, sl_rows, sl_meta, sl_rec, su_rows, su_meta,
             su_rec, pos_l, pos_u, y_t, x_t, lvl_tiles, lvl_cnt, status, ps_rec, ps_info, ps_part, ps_idx,
-            ps_vmap, ps_posl, ps_bperm, ps_yu, total;
+            ps_vmap, ps_posl, ps_bperm, ps_yu, gs_part, gs_rec, gs_lo, gs_cols, gs_stream, gs_y, total;
     } off{};
     // bound device pointers
     unsigned char *ws = nullptr;
@@ -282,6 +323,10 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm);
 int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts);
 double psweep_estimate_us(const Plan &p, const Partition &pt);
 bool detect_grid(const Plan &p, int64_t g[3]);
+void partition_grid_columns(const Plan &p, int P, const int64_t g[3], Partition &pt);   // (y, z) column parts
+// grid sweep planner (gsweep.cu): BILUK_OK, or BILUK_EUNSUPPORTED when the
+// pattern is not a 7-point ILU(0) grid the engine handles
+int plan_gsweep(Plan &p, int num_sms, size_t smem_per_block);
 int op_analyse(Op &o, int32_t bs, int64_t n, int64_t ncols, const int64_t *rp, const int64_t *ci);
 
 }  // namespace biluk

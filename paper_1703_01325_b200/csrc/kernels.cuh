@@ -57,6 +57,29 @@ struct PSweepArgs {
     double *y_u;                 // y in U'-position order (written by the L sweep, read by U' records)
     int nowait;                  // diagnostics: take every dependency's first load as is (wrong results)
 };
+// grid sweep (gsweep.cu)
+struct GSweepArgs {
+    const GPart *parts;
+    const GRec *recs;
+    const int32_t *cols;         // P * 128: (y << 16) | z
+    const unsigned char *stream; // record bytes
+    const double *b;             // right-hand side (n*bs, natural order)
+    double *y;                   // y (n*bs, natural order; written by L, read by U')
+    double *out;                 // x (natural order; may be null)
+    double *y_t;                 // parity-tagged rows (natural index, tag_stride(bs) doubles each)
+    double *x_t;
+    DevStatus *st;
+    const int *skip_flag;
+    uint64_t timeout_ns;
+    int64_t nx, ny, nz;
+    int slot_bytes, kslots;
+    unsigned long long *trace;   // optional: 8 x u64 per record (globaltimer stamps, gsweep.cu), then clock64 stages
+    int64_t nrec_total;
+};
+cudaError_t launch_gsweep(const Plan &p, const GSweepArgs &a, cudaStream_t s);
+cudaError_t gsweep_occupancy(const Plan &p, int *blocks_per_sm);
+cudaError_t launch_gpack(const Plan &p, cudaStream_t s);
+size_t gsweep_smem_bytes(const Plan &p);
 cudaError_t launch_ppack(const Plan &p, cudaStream_t s);
 cudaError_t launch_permute_b(const Plan &p, const double *b, cudaStream_t s, const int *skip = nullptr);
 cudaError_t launch_psweep(const Plan &p, const PSweepArgs &a, cudaStream_t s);

@@ -342,7 +342,12 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     // sweep launch: one CTA per SM holding as many warps as the double-buffered
     // tile ring allows (each warp owns `stages` stage buffers of the largest record)
     p.num_sms = num_sms;
-    if (p.engine == 1) {
+    if (p.engine == 2) {
+        p.sweep_ctas = p.gs.P;
+        p.sweep_warps = 12 + 1 + 3;   // compute groups, producer, halo warps (gsweep.cu)
+        p.sweep_stages = p.gs.kslots;
+        p.stage_bytes = p.gs.slot_bytes;
+    } else if (p.engine == 1) {
         p.sweep_ctas = p.ps.P;
         p.sweep_warps = p.ps.groups * p.ps.nthreads / 32 + p.ps.nprod;   // compute groups + producers
         p.sweep_stages = PS_KSLOTS;
@@ -399,6 +404,13 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.ps_posl = take(ps_on ? 4 * p.n : 0);                               // L position -> row
     p.off.ps_bperm = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);        // b in L-position order
     p.off.ps_yu = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);           // y in U'-position order
+    const bool gs_on = p.engine == 2;
+    p.off.gs_part = take(gs_on ? sizeof(GPart) * p.gs.part.size() : 0);
+    p.off.gs_rec = take(gs_on ? sizeof(GRec) * p.gs.rec.size() : 0);
+    p.off.gs_lo = take(gs_on ? 4 * p.gs.rec_lo.size() : 0);
+    p.off.gs_cols = take(gs_on ? 4 * p.gs.cols.size() : 0);
+    p.off.gs_stream = take(gs_on ? uint64_t(p.gs.stream_bytes) : 0);
+    p.off.gs_y = take(gs_on ? 8 * p.n * p.bs : 0);                          // y in natural order
     p.off.total = o;
 }
 

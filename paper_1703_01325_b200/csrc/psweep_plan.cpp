@@ -320,6 +320,8 @@ void build_part_records(const Plan &p, const Partition &pt, const std::vector<in
 
 }  // namespace
 
+void partition_grid_columns(const Plan &p, int P, const int64_t g[3], Partition &pt) { partition_columns(p, P, g, pt); }
+
 // ---------------------------------------------------------------------------
 // Natural-order structured grid (nx, ny, nz) behind the block pattern of A, if
 // any: the offsets 1, nx and nx*ny must each occur in >= n/4 rows.  Only the

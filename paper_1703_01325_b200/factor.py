@@ -132,7 +132,7 @@ class BlockIlukFactors:
         from .device import torch
         t = torch()
         inf = self.info
-        if inf["engine"] == 1:   # partitioned sweep: 8 stamps per record (see csrc/psweep.cu)
+        if inf["engine"] >= 1:   # partitioned / grid sweep: 8 stamps per record (csrc/psweep.cu, gsweep.cu)
             self._trace = t.zeros((inf["records"] + 16384, 8), dtype=t.int64, device="cuda")
         else:
             self._trace = t.zeros((inf["tiles_L"] + inf["tiles_U"], 4), dtype=t.int64, device="cuda")

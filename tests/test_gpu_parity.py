@@ -285,6 +285,37 @@ def test_both_engines_match_oracle_and_are_repeatable(b2, monkeypatch, engine, c
     f.status()
 
 
+@pytest.mark.parametrize("shape", [(5, 4, 3, 3), (16, 16, 16, 3), (17, 9, 13, 2), (24, 20, 16, 4), (20, 20, 20, 1),
+                                   (33, 7, 5, 3)])
+def test_grid_sweep_matches_oracle(b2, monkeypatch, shape):
+    """The grid sweep (engine 2, opt-in: ILU(0) of a 7-point block grid) against
+    the oracle, bitwise repeatable, on odd shapes and every block size it takes."""
+    import torch
+    monkeypatch.setenv("BILUK_ENGINE", "2")
+    nx, ny, nz, bs = shape
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(nx, ny, nz, bs, seed=7)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0)
+    assert f.info["engine"] == 2
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, 0)
+    rhs = np.random.default_rng(4).standard_normal(n * bs)
+    assert rel_err(b2.apply_preconditioner(f, rhs), of.apply(rhs)) <= TOL
+    rt = torch.from_numpy(rhs).cuda()
+    x1 = b2.apply_preconditioner(f, rt)
+    for _ in range(3):
+        assert torch.equal(b2.apply_preconditioner(f, rt), x1)
+    f.status()
+
+
+def test_grid_sweep_declines_other_patterns(b2, monkeypatch):
+    """Engine 2 is only planned for a 7-point ILU(0) grid: fill or a random
+    pattern falls back to the partitioned sweep."""
+    monkeypatch.setenv("BILUK_ENGINE", "2")
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(8, 8, 8, 3, seed=1)
+    assert b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 1).info["engine"] == 1
+    n, bs, rp, ci, vals = _random_pattern_matrix(200, 3, seed=2)
+    assert b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0).info["engine"] == 1
+
+
 @pytest.mark.parametrize("groups,nprod", [(3, 1), (2, 2), (2, 1), (3, 2)])
 @pytest.mark.parametrize("case", ["grid16_b3_k0", "grid12_b3_k2", "grid10_b4_k1", "rand300_b3_k1"])
 def test_partitioned_kernel_variants_match_oracle(b2, monkeypatch, groups, nprod, case):
