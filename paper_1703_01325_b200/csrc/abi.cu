@@ -479,7 +479,6 @@ static int apply_launch(biluk_plan_t *plan, const double *dev_b, double *dev_x, 
         a.nrec_total = int64_t(p.ps.rec.size());
         a.b_perm = reinterpret_cast<double *>(p.ws + p.off.ps_bperm);
         a.y_u = reinterpret_cast<double *>(p.ws + p.off.ps_yu);
-        a.nowait = std::getenv("BILUK_EXP_NOWAIT") ? 1 : 0;   // diagnostics (wrong results)
         CUDA_TRY(launch_permute_b(p, dev_b, static_cast<cudaStream_t>(stream), skip), "apply");
         if (plan->tev[0]) CUDA_TRY(cudaEventRecord(plan->tev[0], static_cast<cudaStream_t>(stream)), "apply");
         CUDA_TRY(launch_psweep(p, a, static_cast<cudaStream_t>(stream)), "apply");

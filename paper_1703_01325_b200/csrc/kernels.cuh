@@ -55,7 +55,6 @@ struct PSweepArgs {
     int64_t nrec_total;
     const double *b_perm;        // b in L-position order (pvs doubles per position; launch_permute_b)
     double *y_u;                 // y in U'-position order (written by the L sweep, read by U' records)
-    int nowait;                  // diagnostics: take every dependency's first load as is (wrong results)
 };
 // grid sweep (gsweep.cu)
 struct GSweepArgs {

@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                     if (!loaded) ld_tagged<BS>(src, dv);
                     uint64_t t0 = 0;
                     uint32_t spins = 0;
-                    while (!a.nowait && !row_ready<BS>(dv, par)) {
+                    while (!row_ready<BS>(dv, par)) {
                         if (ps_timed_out(t0, spins, a)) {
                             *reinterpret_cast<volatile int *>(&abort_flag) = 1;
                             break;
