@@ -90,6 +90,15 @@ __device__ __forceinline__ int64_t ring_alloc(uint32_t &head, uint32_t tail, int
     return -1;
 }
 
+// a tagged row of 4 words as one 256-bit load (others as ld_tagged)
+template <int BS>
+__device__ __forceinline__ void ld_tagged_wide(const double *p, double (&w)[BS + 1]) {
+    if constexpr (BS + 1 == 4) {
+        ld_relaxed_v4(p, w[0], w[1], w[2], w[3]);
+    } else {
+        ld_tagged<BS>(p, w);
+    }
+}
 __device__ __forceinline__ bool ps_timed_out(uint64_t &t0, uint32_t &spins, const PSweepArgs &a) {
     ++spins;
     if (spins == 1) {
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const double *gvec = up ? a.x_t : a.y_t;
             const bool dneed = gt < ng;
             double dval[BS + 1];
-            if (dneed) ld_tagged<BS>(gvec + size_t(gpos[gt]) * TVS, dval);
+            if (dneed) ld_tagged_wide<BS>(gvec + size_t(gpos[gt]) * TVS, dval);
             // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
             auto init_acc = [&](int q, double (&acc)[BS]) {
                 const double *inp = inp0 + size_t(q) * VS;
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             {
                 auto fetch_dep = [&](int e, double (&dv)[BS + 1], bool loaded) {
                     const double *src = gvec + size_t(gpos[e]) * TVS;
-                    if (!loaded) ld_tagged<BS>(src, dv);
+                    if (!loaded) ld_tagged_wide<BS>(src, dv);
                     uint64_t t0 = 0;
                     uint32_t spins = 0;
                     while (!row_ready<BS>(dv, par)) {
@@ -453,7 +462,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                             *reinterpret_cast<volatile int *>(&abort_flag) = 1;
                             break;
                         }
-                        ld_tagged<BS>(src, dv);
+                        ld_tagged_wide<BS>(src, dv);
                     }
                     double v[BS];
                     untag_row<BS>(dv, v);
