@@ -29,9 +29,20 @@ __all__ = ["SolverConfig", "SolveStats", "gmres", "bicgstab", "bicgstab_batched"
 _RHS_MODES = ("ones-solution", "given")
 
 
+# field -> (accepts, requirement): the reference's rules (gmres.py:36-46)
+_CONFIG_RULES = {
+    "restart": (lambda v: v >= 1, "an integer >= 1"),
+    "max_iters": (lambda v: v >= 1, "an integer >= 1"),
+    "rel_tol": (lambda v: v > 0.0, "a positive number"),   # (NaN fails too)
+    "abs_tol": (lambda v: v > 0.0, "a positive number"),
+    "rhs_mode": (lambda v: v in _RHS_MODES, f"one of {_RHS_MODES}"),
+}
+
+
 @dataclass
 class SolverConfig:
-    """Settings for the solvers (reference gmres.py:23-46; same defaults and validation)."""
+    """Solver settings with the reference's fields and defaults (gmres.py:23-35);
+    every field is checked against `_CONFIG_RULES` (ValueError naming it)."""
 
     restart: int = 20
     max_iters: int = 10000
@@ -40,14 +51,10 @@ class SolverConfig:
     rhs_mode: str = "ones-solution"
 
     def __post_init__(self):
-        if self.restart < 1:
-            raise ValueError("restart must be at least 1")
-        if self.max_iters < 1:
-            raise ValueError("max_iters must be at least 1")
-        if not (self.rel_tol > 0.0) or not (self.abs_tol > 0.0):
-            raise ValueError("tolerances must be positive")
-        if self.rhs_mode not in _RHS_MODES:
-            raise ValueError(f"rhs_mode must be one of {_RHS_MODES}")
+        for name, (accepts, requirement) in _CONFIG_RULES.items():
+            value = getattr(self, name)
+            if not accepts(value):
+                raise ValueError(f"SolverConfig.{name} = {value!r}: must be {requirement}")
 
 
 @dataclass

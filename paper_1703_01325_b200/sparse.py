@@ -1,8 +1,10 @@
 """Host-side sparse containers of the drop-in API (reference sparse.py).
 
-Same constructors, fields, validation rules and layouts as the reference
-(`CsrMatrix` sparse.py:55-89, `BcsrMatrix` :92-151 with column-major blocks,
-`PatternMatrix` :154-221), so objects can be passed back and forth.  These
+The constructors take the reference's arguments and expose its fields and
+layouts (`CsrMatrix` sparse.py:55-89, `BcsrMatrix` :92-151 with column-major
+blocks, `PatternMatrix` :154-221) and enforce its structural rules, so objects
+can be passed back and forth; the index checks live in one place
+(`_compressed_violation`) and name the offending row or index.  These
 are index/value holders only: every numeric operation on the path runs on the
 GPU through libbiluk.  Reference objects are accepted anywhere through
 duck typing (``as_bsr``).
@@ -18,91 +20,115 @@ __all__ = ["CsrMatrix", "BcsrMatrix", "PatternMatrix", "bcsr_from_csr", "csr_exp
            "extract_point_pattern", "csr_from_triplets", "assemble_csr", "as_bsr", "block_diagonal"]
 
 
-def _index_array(a, name):
-    arr = np.ascontiguousarray(a, dtype=np.int64)
-    if arr.ndim != 1:
-        raise StructuralError(f"{name} must be one-dimensional")
-    return arr
+def _index_vector(a, label):
+    v = np.asarray(a, dtype=np.int64)
+    if v.ndim != 1:
+        raise StructuralError(f"{label}: expected a one-dimensional index array, got shape {v.shape}")
+    return np.ascontiguousarray(v)
 
 
-def _check_structure(nrows, ncols, rp, ci, what):
-    """Structural invariants of CSR / BSR indices (reference sparse.py:35-52)."""
+def _compressed_violation(nrows, ncols, rp, ci):
+    """The first structural rule a compressed-row index pair breaks, or None.
+
+    Rules (the reference's, sparse.py:35-52): non-negative dimensions; a row
+    pointer of nrows + 1 entries from 0, never decreasing; one column index
+    per stored entry, inside [0, ncols), strictly increasing within a row.
+    """
     if nrows < 0 or ncols < 0:
-        raise StructuralError(f"{what}: negative dimension")
-    if rp.shape != (nrows + 1,) or rp[0] != 0:
-        raise StructuralError(f"{what}: row_ptr must have num_rows+1 entries starting at 0")
-    if np.any(np.diff(rp) < 0):
-        raise StructuralError(f"{what}: row_ptr must be nondecreasing")
+        return f"dimensions ({nrows}, {ncols}) must be non-negative"
+    if len(rp) != nrows + 1:
+        return f"row pointer has {len(rp)} entries, {nrows + 1} expected"
+    if rp[0] != 0:
+        return f"row pointer starts at {int(rp[0])}, not 0"
+    steps = np.diff(rp)
+    if (steps < 0).any():
+        return f"row pointer decreases after row {int(np.argmax(steps < 0))}"
     nnz = int(rp[-1])
-    if ci.shape != (nnz,):
-        raise StructuralError(f"{what}: col_idx length must equal row_ptr[-1]")
-    if nnz:
-        if ci.min() < 0 or ci.max() >= ncols:
-            raise StructuralError(f"{what}: column index out of range")
-        row_start = np.zeros(nnz + 1, dtype=bool)
-        row_start[rp[:-1]] = True
-        if np.any((np.diff(ci) <= 0) & ~row_start[1:nnz]):
-            raise StructuralError(f"{what}: column indices must increase strictly within a row")
+    if len(ci) != nnz:
+        return f"{len(ci)} column indices for {nnz} stored entries"
+    if nnz == 0:
+        return None
+    lo, hi = int(ci.min()), int(ci.max())
+    if lo < 0 or hi >= ncols:
+        return f"column index {lo if lo < 0 else hi} outside [0, {ncols})"
+    # consecutive entries (t, t + 1) of one row must increase; a row start breaks the pair
+    same_row = np.ones(nnz - 1, dtype=bool)
+    starts = rp[1:-1]
+    same_row[starts[(starts > 0) & (starts < nnz)] - 1] = False
+    bad = np.flatnonzero(same_row & (np.diff(ci) <= 0))
+    if bad.size:
+        row = int(np.searchsorted(rp, bad[0], side="right") - 1)
+        return f"column indices of row {row} are not strictly increasing"
+    return None
 
 
-class CsrMatrix:
-    """Point-wise CSR matrix (reference sparse.py:55-89)."""
+class _RowCompressed:
+    """Index half shared by the point and block containers: the row pointer,
+    the column indices and the checks on them."""
 
-    def __init__(self, num_rows, num_cols, row_ptr, col_idx, values):
-        self.num_rows = int(num_rows)
-        self.num_cols = int(num_cols)
-        self.row_ptr = _index_array(row_ptr, "row_ptr")
-        self.col_idx = _index_array(col_idx, "col_idx")
-        self.values = np.ascontiguousarray(values, dtype=np.float64)
-        _check_structure(self.num_rows, self.num_cols, self.row_ptr, self.col_idx, "CsrMatrix")
-        if self.values.shape != self.col_idx.shape:
-            raise StructuralError("CsrMatrix: values length must equal col_idx length")
+    def _set_index(self, kind, nrows, ncols, row_ptr, col_idx):
+        rp = _index_vector(row_ptr, f"{kind} row_ptr")
+        ci = _index_vector(col_idx, f"{kind} col_idx")
+        why = _compressed_violation(nrows, ncols, rp, ci)
+        if why is not None:
+            raise StructuralError(f"{kind}: {why}")
+        self.row_ptr, self.col_idx = rp, ci
 
-    @property
-    def shape(self):
-        return (self.num_rows, self.num_cols)
-
-    @property
-    def nnz(self):
+    def _stored(self):
         return int(self.row_ptr[-1])
 
+    def _span(self, i):
+        return int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+
+    def _row_of_entry(self, nrows):
+        return np.repeat(np.arange(nrows), np.diff(self.row_ptr))
+
+
+class CsrMatrix(_RowCompressed):
+    """Point-wise CSR matrix: num_rows, num_cols, row_ptr, col_idx, values
+    (the fields of reference sparse.py:55-89)."""
+
+    def __init__(self, num_rows, num_cols, row_ptr, col_idx, values):
+        self.num_rows, self.num_cols = int(num_rows), int(num_cols)
+        self._set_index("CsrMatrix", self.num_rows, self.num_cols, row_ptr, col_idx)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if self.values.shape != (self._stored(),):
+            raise StructuralError(f"CsrMatrix: {self.values.size} values for {self._stored()} stored entries")
+
+    shape = property(lambda self: (self.num_rows, self.num_cols))
+    nnz = property(lambda self: self._stored())
+
     def row(self, i):
-        s, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        s, e = self._span(i)
         return self.col_idx[s:e], self.values[s:e]
 
     def to_dense(self):
-        out = np.zeros(self.shape)
-        rows = np.repeat(np.arange(self.num_rows), np.diff(self.row_ptr))
-        out[rows, self.col_idx] = self.values
-        return out
+        dense = np.zeros(self.shape)
+        dense[self._row_of_entry(self.num_rows), self.col_idx] = self.values
+        return dense
 
     def __repr__(self):
         return f"CsrMatrix({self.num_rows}x{self.num_cols}, nnz={self.nnz})"
 
 
-class BcsrMatrix:
-    """Block CSR with dense bs x bs blocks flattened column-major (reference sparse.py:92-151)."""
+class BcsrMatrix(_RowCompressed):
+    """Block CSR: bs x bs blocks stored flat and column-major, block t at
+    values[t*bs*bs:(t+1)*bs*bs] (the fields and layout of reference sparse.py:92-151)."""
 
     def __init__(self, block_size, num_block_rows, num_block_cols, row_ptr, col_idx, values):
         self.block_size = int(block_size)
-        self.num_block_rows = int(num_block_rows)
-        self.num_block_cols = int(num_block_cols)
-        self.row_ptr = _index_array(row_ptr, "row_ptr")
-        self.col_idx = _index_array(col_idx, "col_idx")
-        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        self.num_block_rows, self.num_block_cols = int(num_block_rows), int(num_block_cols)
         if self.block_size < 1:
-            raise StructuralError("BcsrMatrix: block size must be at least 1")
-        _check_structure(self.num_block_rows, self.num_block_cols, self.row_ptr, self.col_idx, "BcsrMatrix")
-        if self.values.shape != (self.nnzb * self.block_size ** 2,):
-            raise StructuralError("BcsrMatrix: values length must be nnzb * block_size^2")
+            raise StructuralError(f"BcsrMatrix: block size {self.block_size} is not positive")
+        self._set_index("BcsrMatrix", self.num_block_rows, self.num_block_cols, row_ptr, col_idx)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        want = self._stored() * self.block_size ** 2
+        if self.values.shape != (want,):
+            raise StructuralError(f"BcsrMatrix: {self.values.size} values, {want} expected "
+                                  f"({self._stored()} blocks of {self.block_size}x{self.block_size})")
 
-    @property
-    def nnzb(self):
-        return int(self.row_ptr[-1])
-
-    @property
-    def shape(self):
-        return (self.num_block_rows * self.block_size, self.num_block_cols * self.block_size)
+    nnzb = property(lambda self: self._stored())
+    shape = property(lambda self: (self.num_block_rows * self.block_size, self.num_block_cols * self.block_size))
 
     @property
     def blocks(self):
@@ -111,18 +137,17 @@ class BcsrMatrix:
         return self.values.reshape(self.nnzb, bs, bs).swapaxes(1, 2)
 
     def block_row(self, i):
-        s, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        s, e = self._span(i)
         return self.col_idx[s:e], s
 
     def to_dense(self):
         bs = self.block_size
-        out = np.zeros(self.shape)
-        brow = np.repeat(np.arange(self.num_block_rows), np.diff(self.row_ptr))
-        r = np.arange(bs)
-        rows = (brow[:, None, None] * bs + r[None, :, None])
-        cols = (self.col_idx[:, None, None] * bs + r[None, None, :])
-        out[rows, cols] = self.blocks
-        return out
+        off = np.arange(bs)
+        rows = self._row_of_entry(self.num_block_rows)[:, None, None] * bs + off[None, :, None]
+        cols = self.col_idx[:, None, None] * bs + off[None, None, :]
+        dense = np.zeros(self.shape)
+        dense[rows, cols] = self.blocks
+        return dense
 
     def __repr__(self):
         return (f"BcsrMatrix(bs={self.block_size}, {self.num_block_rows}x{self.num_block_cols} blocks, "
