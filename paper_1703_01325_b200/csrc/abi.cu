@@ -2,6 +2,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -175,7 +177,11 @@ int biluk_plan_create_ex(int32_t bs, int64_t n, const int64_t *row_ptr, const in
         }
     }
     if (P.engine == 1) {
+        const auto t_ps = std::chrono::steady_clock::now();
         rc = plan_psweep(P, sms, size_t(smem), 0);
+        if (std::getenv("BILUK_PLAN_TIMING"))
+            std::fprintf(stderr, "[plan] partitioned sweep records %.3f s\n",
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t_ps).count());
         const double per_part = P.ps.P > 0 ? double(P.ps.rec.size()) / P.ps.P : 0.0;
         const double limit = k >= 1 ? 1500.0 : (bs <= 3 ? 1e30 : 400.0);
         // three compute groups (blocks read at the products) measured faster

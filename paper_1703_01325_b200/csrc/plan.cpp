@@ -8,6 +8,9 @@
 //   materialize (indices)  factor.py:83-121    (A slot -> P' slot map)
 //   build_level_schedule   trisolve.py:98-118  (block granularity for execution)
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -32,6 +35,18 @@ namespace biluk {
 int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,
                    std::vector<int32_t> &out_ci, int64_t *err_row) {
     if (k < 0) return fail(BILUK_EARG, "fill level k must be nonnegative");
+    if (k == 0) {
+        // ILU(0): every entry of A has level 0 and nothing fills in -- the
+        // pattern is A's, once every row is known to hold its diagonal
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::binary_search(ci + rp[i], ci + rp[i + 1], int32_t(i))) {
+                if (err_row) *err_row = i;
+                return fail(BILUK_ESTRUCT, "row " + std::to_string(i) + " has no diagonal entry");
+            }
+        out_rp.assign(rp, rp + n + 1);
+        out_ci.assign(ci, ci + rp[n]);
+        return BILUK_OK;
+    }
     std::vector<int32_t> lev(n, -1);
     std::vector<int64_t> up_ptr(n + 1, 0);
     std::vector<int32_t> up_col;
@@ -215,7 +230,11 @@ int plan_analyse(Plan &p, int32_t bs, int64_t n, const int64_t *rp, const int64_
     }
     for (int64_t i = 0; i <= n; ++i) p.a_rp[i] = int32_t(rp[i]);
 
+    const auto t_sym = std::chrono::steady_clock::now();
     int rc = symbolic_phase(n, p.a_rp.data(), p.a_ci.data(), k, p.p_rp, p.p_ci, err_row);
+    if (std::getenv("BILUK_PLAN_TIMING"))
+        std::fprintf(stderr, "[plan] symbolic %.3f s\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t_sym).count());
     if (rc != BILUK_OK) return rc;
     p.nnzP = p.p_rp[n];
     p.p_diag.resize(n);

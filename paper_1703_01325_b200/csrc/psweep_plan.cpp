@@ -8,6 +8,7 @@
 // CTA per part, and the records a CTA streams are laid out back to back.
 // Integer work only; the values are packed on the device (ppack_kernel).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -515,33 +516,45 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     // concatenated: offsets inside a part are relative until the merge
     std::vector<PartRecords> built(P);
     parallel_parts(P, [&](int c) { build_part_records(p, pt, ordL[c], ordU[c], c, built[c]); });
-    ps.rec.clear();
-    ps.idx.clear();
-    ps.vmap.clear();
+    // concatenate: every part's share of the record, index and value-map
+    // arrays is known up front, so the parts are copied into place in parallel
     ps.part_rec.assign(P + 1, 0);
     std::vector<int32_t> part_nl(P, 0);   // L records of each part
+    std::vector<int64_t> base_rec(P + 1, 0), base_bytes(P + 1, 0), base_idx(P + 1, 0), base_vmap(P + 1, 0);
     ps.rec_total = ps.max_rec = ps.max_glob = ps.nglob_total = 0;
     ps.nlrec_max = 0;
     for (int c = 0; c < P; ++c) {
-        PartRecords &pr = built[c];
+        const PartRecords &pr = built[c];
         if (pr.rc != BILUK_OK) return fail(pr.rc, pr.msg);
-        ps.part_rec[c] = int32_t(ps.rec.size());
+        ps.part_rec[c] = int32_t(base_rec[c]);
         part_nl[c] = pr.nl;
         ps.nlrec_max = std::max<int32_t>(ps.nlrec_max, pr.nl);
-        for (PRecInfo info : pr.rec) {
-            info.off += uint64_t(ps.rec_total);
-            info.idx_off += uint64_t(ps.idx.size());
-            info.vmap_off += int64_t(ps.vmap.size());
-            ps.rec.push_back(info);
-        }
-        ps.rec_total += pr.rec_total;
+        base_rec[c + 1] = base_rec[c] + int64_t(pr.rec.size());
+        base_bytes[c + 1] = base_bytes[c] + pr.rec_total;
+        base_idx[c + 1] = base_idx[c] + int64_t(pr.idx.size());
+        base_vmap[c + 1] = base_vmap[c] + int64_t(pr.vmap.size());
         ps.max_rec = std::max(ps.max_rec, pr.max_rec);
         ps.max_glob = std::max(ps.max_glob, pr.max_glob);
         ps.nglob_total += pr.nglob_total;
-        ps.idx.insert(ps.idx.end(), pr.idx.begin(), pr.idx.end());
-        ps.vmap.insert(ps.vmap.end(), pr.vmap.begin(), pr.vmap.end());
-        pr = PartRecords();   // free as we go
     }
+    ps.rec_total = base_bytes[P];
+    ps.rec.resize(size_t(base_rec[P]));
+    ps.idx.resize(size_t(base_idx[P]));
+    ps.vmap.resize(size_t(base_vmap[P]));
+    parallel_parts(P, [&](int c) {
+        PartRecords &pr = built[c];
+        PRecInfo *dst = ps.rec.data() + base_rec[c];
+        for (size_t r = 0; r < pr.rec.size(); ++r) {
+            PRecInfo info = pr.rec[r];
+            info.off += uint64_t(base_bytes[c]);
+            info.idx_off += uint64_t(base_idx[c]);
+            info.vmap_off += base_vmap[c];
+            dst[r] = info;
+        }
+        std::copy(pr.idx.begin(), pr.idx.end(), ps.idx.begin() + base_idx[c]);
+        std::copy(pr.vmap.begin(), pr.vmap.end(), ps.vmap.begin() + base_vmap[c]);
+        pr = PartRecords();   // free as we go
+    });
     ps.part_rec[P] = int32_t(ps.rec.size());
     ps.part_rec.insert(ps.part_rec.end(), part_nl.begin(), part_nl.end());   // then P L-record counts
     if (ps.rec.size() >= size_t(INT32_MAX)) return fail(BILUK_EUNSUPPORTED, "too many sweep records");
