@@ -8,6 +8,9 @@
 //   materialize (indices)  factor.py:83-121    (A slot -> P' slot map)
 //   build_level_schedule   trisolve.py:98-118  (block granularity for execution)
 #include <algorithm>
+#include <string>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -32,9 +35,11 @@ namespace biluk {
 // same integer arithmetic.  `upper` keeps, per finalized row, its (col, level)
 // pairs right of the diagonal (:44-45, :70-71).
 // ---------------------------------------------------------------------------
-int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,
-                   std::vector<int32_t> &out_ci, int64_t *err_row) {
-    if (k < 0) return fail(BILUK_EARG, "fill level k must be nonnegative");
+// the reference's row-merge order, row after row (each row merges the
+// finished upper rows it references): kept as the cross-check of the
+// row-parallel form below (BILUK_SYMBOLIC=sequential)
+static int symbolic_phase_rows(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,
+                               std::vector<int32_t> &out_ci, int64_t *err_row) {
     if (k == 0) {
         // ILU(0): every entry of A has level 0 and nothing fills in -- the
         // pattern is A's, once every row is known to hold its diagonal
@@ -109,6 +114,110 @@ int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::
             return fail(BILUK_EUNSUPPORTED, "ILU(k) pattern exceeds 2^31 blocks");
         out_rp[i + 1] = int32_t(out_ci.size());
         up_ptr[i + 1] = int64_t(up_col.size());
+    }
+    return BILUK_OK;
+}
+
+// Row-parallel form.  The level of entry (i, j) is the length minus one of
+// the shortest path i -> ... -> j in the graph of A whose intermediate
+// vertices are all smaller than min(i, j) (the characterisation the row
+// merge above computes incrementally: split any such path at its largest
+// intermediate p and both halves are entries of rows i and p).  So every
+// row is found on its own: breadth-first layers of path length 1 .. k+1,
+// each vertex keeping the smallest possible largest-intermediate over paths
+// of that length (min of max composes layer by layer); j joins the row at
+// the first length whose bound is below min(i, j).  Rows are split over the
+// host cores; the result is bit-identical to the row merge (tests compare
+// both on grids and random patterns, and the goldens pin the reference).
+int symbolic_phase(int64_t n, const int32_t *rp, const int32_t *ci, int k, std::vector<int32_t> &out_rp,
+                   std::vector<int32_t> &out_ci, int64_t *err_row) {
+    if (k < 0) return fail(BILUK_EARG, "fill level k must be nonnegative");
+    const char *mode = std::getenv("BILUK_SYMBOLIC");
+    if (k == 0 || (mode && std::string(mode) == "sequential") || n < 4096)
+        return symbolic_phase_rows(n, rp, ci, k, out_rp, out_ci, err_row);
+    unsigned nt = std::thread::hardware_concurrency();
+    if (const char *e = std::getenv("BILUK_PLAN_THREADS")) nt = unsigned(std::max(1, std::atoi(e)));
+    nt = std::max(1u, std::min(nt, 64u));
+    const int64_t nblk = std::min<int64_t>(int64_t(nt) * 16, n);
+    std::vector<std::vector<int32_t>> cols(nblk);          // each block's rows, concatenated
+    std::vector<std::vector<int32_t>> lens(nblk);          // their lengths
+    std::vector<int64_t> bad(nblk, -1);                     // first row without a diagonal
+    std::atomic<int64_t> next{0};
+    auto work = [&]() {
+        std::vector<std::pair<int32_t, int32_t>> cur, nxt, res;   // (vertex, bound) / (vertex, length)
+        for (int64_t b = next++; b < nblk; b = next++) {
+            const int64_t i0 = n * b / nblk, i1 = n * (b + 1) / nblk;
+            std::vector<int32_t> &out = cols[b];
+            std::vector<int32_t> &ln = lens[b];
+            ln.reserve(size_t(i1 - i0));
+            for (int64_t i = i0; i < i1; ++i) {
+                const int32_t ii = int32_t(i);
+                cur.clear();
+                res.clear();
+                bool diag = false;
+                for (int32_t t = rp[i]; t < rp[i + 1]; ++t) {
+                    const int32_t j = ci[t];
+                    if (j == ii) {
+                        diag = true;
+                        continue;
+                    }
+                    res.emplace_back(j, 1);
+                    cur.emplace_back(j, -1);   // no intermediate yet
+                }
+                if (!diag) {
+                    bad[b] = i;
+                    break;
+                }
+                for (int len = 2; len <= k + 1 && !cur.empty(); ++len) {
+                    nxt.clear();
+                    for (const auto &vm : cur) {
+                        const int32_t v = vm.first;
+                        if (v >= ii) continue;   // only smaller vertices are intermediates
+                        const int32_t bound = std::max(vm.second, v);
+                        for (int32_t t = rp[v]; t < rp[v + 1]; ++t)
+                            if (ci[t] != ii && ci[t] != v) nxt.emplace_back(ci[t], bound);
+                    }
+                    std::sort(nxt.begin(), nxt.end());
+                    cur.clear();
+                    for (size_t a = 0; a < nxt.size(); ++a)
+                        if (a == 0 || nxt[a].first != nxt[a - 1].first) cur.push_back(nxt[a]);   // smallest bound
+                    for (const auto &wm : cur)
+                        if (wm.second < std::min(ii, wm.first)) res.emplace_back(wm.first, len);
+                }
+                res.emplace_back(ii, 0);
+                std::sort(res.begin(), res.end());
+                int32_t cnt = 0;
+                for (size_t a = 0; a < res.size(); ++a)
+                    if (a == 0 || res[a].first != res[a - 1].first) {
+                        out.push_back(res[a].first);
+                        ++cnt;
+                    }
+                ln.push_back(cnt);
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (std::thread &t : pool) t.join();
+    for (int64_t b = 0; b < nblk; ++b)
+        if (bad[b] >= 0) {
+            if (err_row) *err_row = bad[b];
+            return fail(BILUK_ESTRUCT, "row " + std::to_string(bad[b]) + " has no diagonal entry");
+        }
+    int64_t total = 0;
+    for (int64_t b = 0; b < nblk; ++b) total += int64_t(cols[b].size());
+    if (total > int64_t(INT32_MAX)) return fail(BILUK_EUNSUPPORTED, "ILU(k) pattern exceeds 2^31 blocks");
+    out_rp.assign(n + 1, 0);
+    out_ci.resize(size_t(total));
+    int64_t row = 0, at = 0;
+    for (int64_t b = 0; b < nblk; ++b) {
+        for (int32_t c : lens[b]) {
+            out_rp[row + 1] = out_rp[row] + c;
+            ++row;
+        }
+        std::copy(cols[b].begin(), cols[b].end(), out_ci.begin() + at);
+        at += int64_t(cols[b].size());
+        std::vector<int32_t>().swap(cols[b]);
     }
     return BILUK_OK;
 }
