@@ -443,6 +443,13 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     PSweep &ps = p.ps;
     const int bs = p.bs, bs2 = bs * bs, vs = ps_vec_stride(bs);
     const int64_t n = p.n;
+    const bool timing = std::getenv("BILUK_PLAN_TIMING") != nullptr;
+    auto last = std::chrono::steady_clock::now();
+    auto tick = [&](const char *what) {   // diagnostics: phase times (BILUK_PLAN_TIMING)
+        const auto now = std::chrono::steady_clock::now();
+        if (timing) std::fprintf(stderr, "[plan]   %s %.3f s\n", what, std::chrono::duration<double>(now - last).count());
+        last = now;
+    };
     // ---- choose the partition ---------------------------------------------------
     // ILU(0) on a structured grid: (y, z) columns.  With fill (k >= 1) a row
     // also depends on rows of the next column over in y (fill entries such as
@@ -514,8 +521,10 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
 
     // the records of every part, built independently (threads), then
     // concatenated: offsets inside a part are relative until the merge
+    tick("partition and row orders");
     std::vector<PartRecords> built(P);
     parallel_parts(P, [&](int c) { build_part_records(p, pt, ordL[c], ordU[c], c, built[c]); });
+    tick("part records");
     // concatenate: every part's share of the record, index and value-map
     // arrays is known up front, so the parts are copied into place in parallel
     ps.part_rec.assign(P + 1, 0);
@@ -555,6 +564,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
         std::copy(pr.vmap.begin(), pr.vmap.end(), ps.vmap.begin() + base_vmap[c]);
         pr = PartRecords();   // free as we go
     });
+    tick("merge");
     ps.part_rec[P] = int32_t(ps.rec.size());
     ps.part_rec.insert(ps.part_rec.end(), part_nl.begin(), part_nl.end());   // then P L-record counts
     if (ps.rec.size() >= size_t(INT32_MAX)) return fail(BILUK_EUNSUPPORTED, "too many sweep records");
