@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gsweep_kernel(const GSweepArgs 
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t full_bar[GS_K];    // record landed
     __shared__ __align__(8) uint64_t empty_bar[GS_K];   // record consumed (every compute thread)
-    __shared__ __align__(8) uint64_t hfull[GS_H];       // halo values of a record stored (every halo warp's lane 0)
+    __shared__ __align__(8) uint64_t hfull[GS_H];       // halo values of a record stored (every lane of its halo warp)
     __shared__ __align__(8) uint64_t hempty[GS_H];      // halo slot consumed (every compute thread)
     __shared__ __align__(8) uint64_t ldone;             // every compute thread's y stores are done
     __shared__ int abort_flag;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gsweep_kernel(const GSweepArgs 
             mbar_init(empty_bar + s, GS_NC);
         }
         for (int h = 0; h < GS_H; ++h) {
-            mbar_init(hfull + h, 1);
+            mbar_init(hfull + h, 32);   // every lane of the serving halo warp
             mbar_init(hempty + h, GS_NC);
         }
         mbar_init(&ldone, GS_G * GS_NC);
@@ -255,11 +255,9 @@ __global__ void __launch_bounds__(GS_THREADS, 1) gsweep_kernel(const GSweepArgs 
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) {
-                if (a.trace) a.trace[size_t(pt.rec0 + r) * 8 + 6] = globaltimer();
-                g_mbar_arrive(hfull + h);
-            }
+            // every lane releases its own stores (one arrival per lane)
+            if (lane == 0 && a.trace) a.trace[size_t(pt.rec0 + r) * 8 + 6] = globaltimer();
+            g_mbar_arrive(hfull + h);
             if (__any_sync(0xffffffffu, !ok)) break;
         }
     } else {
