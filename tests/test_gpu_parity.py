@@ -285,6 +285,25 @@ def test_both_engines_match_oracle_and_are_repeatable(b2, monkeypatch, engine, c
     f.status()
 
 
+@pytest.mark.parametrize("bs", [5, 6, 7, 8])
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_large_blocks_match_oracle(b2, bs, k):
+    """Block sizes 5..8 (the tiled sweep: several lanes per block row) against
+    the oracle, bitwise repeatable."""
+    import torch
+    n, bs, rp, ci, vals = b2.reservoir_block_grid(9, 8, 7, bs, seed=11)
+    f = b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), k)
+    assert f.info["engine"] == 0
+    of = orc.build_preconditioner(n, bs, rp, ci, vals, k)
+    rhs = np.random.default_rng(5).standard_normal(n * bs)
+    assert rel_err(b2.apply_preconditioner(f, rhs), of.apply(rhs)) <= TOL
+    rt = torch.from_numpy(rhs).cuda()
+    x1 = b2.apply_preconditioner(f, rt)
+    for _ in range(2):
+        assert torch.equal(b2.apply_preconditioner(f, rt), x1)
+    f.status()
+
+
 @pytest.mark.parametrize("shape", [(5, 4, 3, 3), (16, 16, 16, 3), (17, 9, 13, 2), (24, 20, 16, 4), (20, 20, 20, 1),
                                    (33, 7, 5, 3)])
 def test_grid_sweep_matches_oracle(b2, monkeypatch, shape):
