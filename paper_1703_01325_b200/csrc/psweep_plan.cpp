@@ -80,9 +80,10 @@ void partition_columns(const Plan &p, int P, const int64_t g[3], Partition &pt) 
     const int64_t nx = g[0], ny = g[1], nz = g[2];
     // as many parts as allowed whose columns fit one record per level (a part
     // of more than 128 columns splits each level into two records: twice the
-    // chain); among those, about twice as many parts along z as along y
-    // (128^3 ILU(0) sweep: 12x12 558 us, 9x16 546, 8x18 543; 10x14 -- 130
-    // columns per part -- 740)
+    // chain); among those, about twice as many parts along z as along y,
+    // ties to the larger pz (128^3 ILU(0) sweep: 12x12 558 us, 11x13 547,
+    // 9x16 540.5, 8x18 537.7 over three runs each; 10x14 -- 130 columns per
+    // part -- 741)
     int best_y = 1, best_z = 1;
     double best = -1e300;
     for (int pz = 1; pz <= std::min<int64_t>(P, nz); ++pz) {
@@ -90,7 +91,7 @@ void partition_columns(const Plan &p, int P, const int64_t g[3], Partition &pt) 
         if (py < 1) continue;
         const int64_t cols = ((ny + py - 1) / py) * ((nz + pz - 1) / pz);
         const double score = (cols <= 128 ? 1e9 : 0.0) + double(py) * pz - 3.0 * std::abs(double(pz) - 2.0 * py);
-        if (score > best) {
+        if (score >= best) {
             best = score;
             best_y = py;
             best_z = pz;
