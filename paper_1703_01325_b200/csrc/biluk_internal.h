@@ -166,8 +166,13 @@ struct PRecInfo {       // 64 bytes: one per record, read by the producer, the g
     int32_t pos0;       // vector position of its first row (inputs: pos0 .. pos0 + nrows)
     int32_t pad[2];
 };
-// doubles per position of the partitioned sweep's vectors (>= 2: 16-byte rows)
+// doubles per position of the partitioned sweep's vector ring (>= 2: 16-byte rows)
 BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
+// the rows' inputs (b in L-position order, y in U'-position order) are packed,
+// bs doubles per position; a record's input area in shared memory holds its
+// rows plus the 8 bytes of slack the bulk copy may start early by (it starts
+// at the 16-byte boundary at or below the first row)
+BILUK_HD constexpr inline int64_t ps_in_bytes(int bs, int nrows) { return (int64_t(nrows) * bs * 8 + 8 + 15) & ~int64_t(15); }
 // fetched dependencies per record (a multiple of 32: one per poll lane and round)
 BILUK_HD constexpr inline int ps_glob_cap(int) { return 1024; }   // fetched dependencies per record (the compute threads loop over them)
 constexpr int PS_KSLOTS = 16;      // records in flight per CTA (mbarrier sets)

@@ -530,8 +530,8 @@ void plan_layout(Plan &p, int num_sms, size_t smem_per_sm) {
     p.off.ps_vmap = take(4 * p.ps.vmap.size());
     const bool ps_on = p.engine == 1;
     p.off.ps_posl = take(ps_on ? 4 * p.n : 0);                               // L position -> row
-    p.off.ps_bperm = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);        // b in L-position order
-    p.off.ps_yu = take(ps_on ? 8 * p.n * ps_vec_stride(p.bs) : 0);           // y in U'-position order
+    p.off.ps_bperm = take(ps_on ? 8 * p.n * p.bs + 16 : 0);                  // b in L-position order (packed)
+    p.off.ps_yu = take(ps_on ? 8 * p.n * p.bs + 16 : 0);                     // y in U'-position order (packed)
     const bool gs_on = p.engine == 2;
     p.off.gs_part = take(gs_on ? sizeof(GPart) * p.gs.part.size() : 0);
     p.off.gs_rec = take(gs_on ? sizeof(GRec) * p.gs.rec.size() : 0);

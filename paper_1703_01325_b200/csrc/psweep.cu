@@ -152,7 +152,7 @@ template <int BS, int G, int NP>
 __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PSweepArgs a) {
     constexpr int PS_NW = G * PS_NG / 32;   // compute warps; then the two producers
     constexpr int BS2 = BS * BS;
-    constexpr int VS = ps_vec_stride(BS);   // input rows (b gathered / y_u)
+    constexpr int VS = ps_vec_stride(BS);   // component planes of the vector ring
     constexpr int TVS = tag_stride(BS);     // tagged rows of y_t / x_t
     constexpr int K = PS_KSLOTS;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -270,12 +270,18 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const int pj = pf - (issued & ~31);   // index into the two windows
             const uint64_t pf_off = __shfl_sync(0xffffffffu, pj < 32 ? cur_off : nxt_off, pj & 31);
             const uint32_t pf_bytes = __shfl_sync(0xffffffffu, pj < 32 ? cur_bytes : nxt_bytes, pj & 31);
-            const uint32_t in_bytes = nr * uint32_t(VS * 8);
+            // packed input rows: the copy starts at the 16-byte boundary at or
+            // below the first row (head = 0 or 8 bytes) and ends on one
+            const uint64_t in_src = uint64_t(pos0) * (BS * 8);
+            const uint32_t head = uint32_t(in_src & 15u);
+            const uint32_t in_bytes = (head + nr * uint32_t(BS * 8) + 15u) & ~15u;
             if (lane == 0) {
                 slot_off[si] = uint32_t(at) + pp * half;
                 mbar_expect_tx(full_bar + si, bytes + in_bytes);
                 bulk_g2s(ring + at, a.recs + off, bytes, full_bar + si, pol);
-                bulk_g2s(ring + at + bytes, (up ? a.y_u : a.b_perm) + size_t(pos0) * VS, in_bytes, full_bar + si, pol);
+                bulk_g2s(ring + at + bytes,
+                         reinterpret_cast<const unsigned char *>(up ? a.y_u : a.b_perm) + (in_src - head), in_bytes,
+                         full_bar + si, pol);
                 if (pf < nk && pj < 64) bulk_prefetch_l2(a.recs + pf_off, pf_bytes);
                 if (a.trace) a.trace[size_t(r0 + rr) * 8 + 0] = globaltimer();
             }
@@ -333,8 +339,8 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const uint32_t vstr = uint32_t(nr) * 8u;
             const uint32_t vb_s = uint32_t(rec + h.vals_off - smem) + (up ? uint32_t(BS2) * vstr : 0u);
             const uint32_t vals_s = vb_s + uint32_t(gt) * 8u;
-            const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off);
-            const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(nr * VS * 8);
+            const double *inp0 = reinterpret_cast<const double *>(rec + h.in_off + ((uint32_t(h.pos0) * (BS * 8)) & 15u));
+            const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(ps_in_bytes(BS, nr));
             // dependencies outside the ring: thread e fetches entry e (tag-polled);
             // the first load is issued here so its round trip overlaps the prep
             const int32_t *gpos = desc + size_t(S) * nr;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             if (dneed) ld_tagged_wide<BS>(gvec + size_t(gpos[gt]) * TVS, dval);
             // accumulator init of row q: b (L) or D^-1 y (U'), both off the chain
             auto init_acc = [&](int q, double (&acc)[BS]) {
-                const double *inp = inp0 + size_t(q) * VS;
+                const double *inp = inp0 + size_t(q) * BS;
                 if (up) {
                     const uint32_t dv_s = vb_s - uint32_t(BS2) * vstr + uint32_t(q) * 8u;
 #pragma unroll
@@ -405,7 +411,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
                         for (int r = 0; r < BS; ++r) a.out[size_t(idx) * BS + r] = acc[r];
                     }
                 } else {
-                    double *yu = a.y_u + size_t(idx) * VS;
+                    double *yu = a.y_u + size_t(idx) * BS;
 #pragma unroll
                     for (int r = 0; r < BS; ++r) yu[r] = acc[r];
                 }
@@ -579,23 +585,16 @@ template <int BS>
 __global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ lrow, const double *__restrict__ b,
                                  double *__restrict__ bp, const int *skip) {
     if (skip && ld_relaxed_s32(skip) != 0) return;
-    // a gather: position p takes b's row lrow[p]; the writes (the costlier
-    // side of a permutation) are coalesced
-    constexpr int VS = ps_vec_stride(BS);
+    // a gather: position p takes b's row lrow[p]; the packed writes (the
+    // costlier side of a permutation) are coalesced
     for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
         const int64_t i = __ldg(lrow + p);
-        double v[VS];
+        double v[BS];
 #pragma unroll
-        for (int c = 0; c < VS; ++c) v[c] = c < BS ? __ldg(b + i * BS + c) : 0.0;
-        double *d = bp + size_t(p) * VS;
-        if constexpr (VS == 4) {
-            reinterpret_cast<double4 *>(d)[0] = make_double4(v[0], v[1], v[2], v[3]);
-        } else if constexpr (VS == 2) {
-            reinterpret_cast<double2 *>(d)[0] = make_double2(v[0], v[1]);
-        } else {
+        for (int c = 0; c < BS; ++c) v[c] = __ldg(b + i * BS + c);
+        double *d = bp + size_t(p) * BS;
 #pragma unroll
-            for (int c = 0; c < VS; ++c) d[c] = v[c];
-        }
+        for (int c = 0; c < BS; ++c) d[c] = v[c];
     }
 }
 

@@ -37,11 +37,12 @@ inline int64_t rec_vals_off(int nrows, int S, int nglob, bool upper) {
 inline int64_t rec_total_bytes(int bs2, int nrows, int S, int nglob, bool upper) {
     return a16(rec_vals_off(nrows, S, nglob, upper) + 8 * int64_t(bs2) * nrows * (S + (upper ? 1 : 0)));
 }
-// shared-memory footprint: the streamed bytes, the inputs (vs doubles per
-// row) and the fetched dependencies (bs doubles each, exact)
+// shared-memory footprint: the streamed bytes, the inputs (ps_in_bytes: bs
+// doubles per row) and the fetched dependencies (bs doubles each, exact)
 inline int64_t rec_foot_bytes(int bs2, int vs, int nrows, int S, int nglob, bool upper) {
     const int bs = int(std::lround(std::sqrt(double(bs2))));
-    return rec_total_bytes(bs2, nrows, S, nglob, upper) + int64_t(nrows) * vs * 8 + a16(int64_t(nglob) * bs * 8);
+    (void)vs;
+    return rec_total_bytes(bs2, nrows, S, nglob, upper) + ps_in_bytes(bs, nrows) + a16(int64_t(nglob) * bs * 8);
 }
 
 inline int32_t nslot_of(const Plan &p, int64_t i, bool upper) {
