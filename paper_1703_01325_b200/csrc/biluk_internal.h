@@ -166,8 +166,9 @@ struct PRecInfo {       // 64 bytes: one per record, read by the producer, the g
     int32_t pos0;       // vector position of its first row (inputs: pos0 .. pos0 + nrows)
     int32_t pad[2];
 };
-// doubles per position of the partitioned sweep's vector ring (>= 2: 16-byte rows)
-BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs <= 2 ? 2 : vec_stride(bs); }
+// component planes of the partitioned sweep's vector ring (component-major:
+// one plane of ring + 2 doubles per component; (ring + 2) * 8 is a multiple of 16)
+BILUK_HD constexpr inline int ps_vec_stride(int bs) { return bs; }
 // the rows' inputs (b in L-position order, y in U'-position order) are packed,
 // bs doubles per position; a record's input area in shared memory holds its
 // rows plus the 8 bytes of slack the bulk copy may start early by (it starts

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     double *vring = reinterpret_cast<double *>(smem);
-    unsigned char *dring = smem + size_t(a.ring_mask + 2) * VS * 8;
+    unsigned char *dring = smem + align128(int64_t(a.ring_mask + 2) * VS * 8);   // the records start 128-aligned
     const int r0 = a.part_rec[blockIdx.x], nrec = a.part_rec[blockIdx.x + 1] - r0;
     const int nlrec = a.part_rec[gridDim.x + 1 + blockIdx.x];   // L records come first
     const uint32_t par = ld_relaxed_u32(&a.st->epoch) & 1u;
@@ -654,7 +654,7 @@ __global__ void ppack_kernel(int64_t nrec, const PRecInfo *__restrict__ info, co
 
 size_t psweep_smem_bytes(const Plan &p) {
     const PSweep &ps = p.ps;
-    return size_t(ps.ring + 2) * ps_vec_stride(p.bs) * 8 + size_t(ps.xval_ring) + size_t(ps.data_ring);
+    return size_t(align128(int64_t(ps.ring + 2) * ps_vec_stride(p.bs) * 8)) + size_t(ps.xval_ring) + size_t(ps.data_ring);
 }
 
 cudaError_t launch_ppack(const Plan &p, cudaStream_t s) {

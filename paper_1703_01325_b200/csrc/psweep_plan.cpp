@@ -503,7 +503,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     // ---- shared-memory budget of one CTA ---------------------------------------
     ps.nthreads = 128;   // rows per record = threads of a compute group
     ps.ring = bs <= 4 ? 512 : 256;
-    const int64_t vring = int64_t(ps.ring + 2) * vs * 8;
+    const int64_t vring = align128(int64_t(ps.ring + 2) * vs * 8);
     ps.xval_ring = 0;   // fetched values live in each record's footprint
     const int64_t budget = int64_t(smem_per_block) - 2048;   // static shared + barriers
     ps.data_ring = ((budget - vring - ps.xval_ring) / 1024) * 1024;
