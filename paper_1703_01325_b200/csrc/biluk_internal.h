@@ -132,8 +132,8 @@ struct Sweep {                       // host copy of one sweep's tile layout
 //                               the U' sweep); U': natural block row (x scatter);
 //                               bit 31: publish the row to the tagged vector (some
 //                               record fetches it)
-//   desc  int32[S][nrows]       >= 0: vector-ring slot (slot `ring` is zero);
-//                               < 0: fetched dependency -(d+1)
+//   desc  int16[S][nrows]       >= 0: vector-ring slot (slot `ring` is zero);
+//                               < 0: fetched dependency -(d+1); padded to a word
 //   gpos  int32[nglob]          deduplicated dependency positions in the
 //                               sweep's own vector (parity-tag polled)
 //   (align 16)

@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const bool up = h.flags & 1;
             const bool live = gt < nr;
             const int32_t *iarr = reinterpret_cast<const int32_t *>(rec + sizeof(PRecHdr));
-            const int32_t *desc = iarr + nr;
+            const int16_t *desc = reinterpret_cast<const int16_t *>(iarr + nr);   // two entries per word
             // block values as 32-bit shared byte offsets: element k of row q of
             // the record's blocks at vb_s + (k * nr + q) * 8 (k = slot * BS2 + e;
             // a U' record's D^-1 blocks precede them)
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(G * PS_NG + 32 * NP, 1) psweep_kernel(const PS
             const uint32_t dep_s = uint32_t(rec + h.in_off - smem) + uint32_t(ps_in_bytes(BS, nr));
             // dependencies outside the ring: thread e fetches entry e (tag-polled);
             // the first load is issued here so its round trip overlaps the prep
-            const int32_t *gpos = desc + size_t(S) * nr;
+            const int32_t *gpos = iarr + nr + (S * nr + 1) / 2;
             const double *gvec = up ? a.x_t : a.y_t;
             const bool dneed = gt < ng;
             double dval[BS + 1];

@@ -27,9 +27,12 @@ namespace {
 inline int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
 // bytes of a record with the given shape (layout: biluk_internal.h)
+// int32 words of a record's index section: header, iarr, desc (int16 entries,
+// two per word), gpos
+inline int64_t rec_desc_words(int nrows, int S) { return (int64_t(S) * nrows + 1) / 2; }
 inline int64_t rec_index_words(int nrows, int S, int nglob, bool upper) {
     (void)upper;
-    return int64_t(sizeof(PRecHdr) / 4) + int64_t(nrows) + int64_t(S) * nrows + nglob;
+    return int64_t(sizeof(PRecHdr) / 4) + int64_t(nrows) + rec_desc_words(nrows, S) + nglob;
 }
 inline int64_t rec_vals_off(int nrows, int S, int nglob, bool upper) {
     return a16(4 * rec_index_words(nrows, S, nglob, upper));
@@ -290,8 +293,8 @@ void build_part_records(const Plan &p, const Partition &pt, const std::vector<in
                 int32_t *w = out.idx.data() + base + sizeof(PRecHdr) / 4;
                 for (int q = 0; q < nr; ++q) w[q] = up ? ord[a + q] : ps.posU[ord[a + q]];
                 w += nr;
-                int32_t *desc = w;
-                int32_t *gpos = w + int64_t(S) * nr;
+                int16_t *desc = reinterpret_cast<int16_t *>(w);
+                int32_t *gpos = w + rec_desc_words(nr, S);
                 for (int t = 0; t < nglob; ++t) gpos[t] = gl[t];
                 const size_t vbase = out.vmap.size();
                 out.vmap.resize(vbase + size_t(S) * nr, -1);
@@ -310,7 +313,7 @@ void build_part_records(const Plan &p, const Partition &pt, const std::vector<in
                             }
                             out.vmap[vbase + size_t(s2) * nr + q] = fs + s2;
                         }
-                        desc[int64_t(s2) * nr + q] = d;
+                        desc[int64_t(s2) * nr + q] = int16_t(d);   // ring slot <= ring, or -(fetched + 1) >= -glob_cap
                     }
                 }
                 out.rec.push_back(info);
@@ -575,7 +578,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     {
         std::vector<uint8_t> need[2] = {std::vector<uint8_t>(n, 0), std::vector<uint8_t>(n, 0)};
         for (const PRecInfo &ri : ps.rec) {
-            const int32_t *gp = ps.idx.data() + ri.idx_off + sizeof(PRecHdr) / 4 + int64_t(ri.nrows) * (1 + ri.S);
+            const int32_t *gp = ps.idx.data() + ri.idx_off + sizeof(PRecHdr) / 4 + ri.nrows + rec_desc_words(ri.nrows, ri.S);
             for (int t = 0; t < ri.nglob; ++t) need[ri.level & 1][gp[t]] = 1;
         }
         for (const PRecInfo &ri : ps.rec) {
@@ -591,7 +594,7 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
         if (std::atoi(env) == 1)
             for (const PRecInfo &ri : ps.rec)
                 if (ri.nglob > 0) {
-                    ps.idx[ri.idx_off + sizeof(PRecHdr) / 4 + int64_t(ri.nrows) * (1 + ri.S)] = ri.pos0;
+                    ps.idx[ri.idx_off + sizeof(PRecHdr) / 4 + ri.nrows + rec_desc_words(ri.nrows, ri.S)] = ri.pos0;
                     break;
                 }
     }
