@@ -505,7 +505,11 @@ int plan_psweep(Plan &p, int num_sms, size_t smem_per_block, int parts) {
     ps.split[1] = pt.split[1];
     // ---- shared-memory budget of one CTA ---------------------------------------
     ps.nthreads = 128;   // rows per record = threads of a compute group
-    ps.ring = bs <= 4 ? 512 : 256;
+    // vector ring rows: two levels of a part suffice for ILU(0) / ILU(1)
+    // (dependencies one level back; the smaller ring leaves the records more
+    // room: 128^3 ILU(0) 515 -> 511 us, ILU(1) 1500 -> 1487 us); ILU(2)+ reach
+    // further back (256 rows measured 34 us slower there)
+    ps.ring = (bs > 4 || p.k <= 1) ? 256 : 512;
     const int64_t vring = align128(int64_t(ps.ring + 2) * vs * 8);
     ps.xval_ring = 0;   // fetched values live in each record's footprint
     const int64_t budget = int64_t(smem_per_block) - 2048;   // static shared + barriers
