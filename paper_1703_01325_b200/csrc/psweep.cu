@@ -586,15 +586,27 @@ __global__ void permute_b_kernel(int64_t n, const int32_t *__restrict__ lrow, co
                                  double *__restrict__ bp, const int *skip) {
     if (skip && ld_relaxed_s32(skip) != 0) return;
     // a gather: position p takes b's row lrow[p]; the packed writes (the
-    // costlier side of a permutation) are coalesced
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t i = __ldg(lrow + p);
-        double v[BS];
+    // costlier side of a permutation) are coalesced.  U positions per thread
+    // and step, their loads issued together (the reads are scattered rows:
+    // latency-bound without several in flight)
+    constexpr int U = 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t p0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p0 < n; p0 += stride * U) {
+        int64_t rows[U];
 #pragma unroll
-        for (int c = 0; c < BS; ++c) v[c] = __ldg(b + i * BS + c);
-        double *d = bp + size_t(p) * BS;
+        for (int u = 0; u < U; ++u) rows[u] = p0 + u * stride < n ? __ldg(lrow + p0 + u * stride) : -1;
+        double v[U][BS];
 #pragma unroll
-        for (int c = 0; c < BS; ++c) d[c] = v[c];
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < BS; ++c) v[u][c] = rows[u] >= 0 ? __ldg(b + rows[u] * BS + c) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (rows[u] >= 0) {
+                double *d = bp + size_t(p0 + u * stride) * BS;
+#pragma unroll
+                for (int c = 0; c < BS; ++c) d[c] = v[u][c];
+            }
     }
 }
 
