@@ -188,11 +188,17 @@ int biluk_plan_create_ex(int32_t bs, int64_t n, const int64_t *row_ptr, const in
         // than two (blocks staged in registers) for every case; BILUK_GROUPS=2
         // selects the two-group kernel
         P.ps.groups = 3;
-        // one producer for large ILU(2)+: its register room stages the blocks
-        // (128^3 ILU(2) 3303 vs 3507 us, 100^3 2138 vs 2192; 64^3 1181 vs 1127,
-        // so small systems keep two); ILU(0) needs both producers (576 vs 714 us)
-        P.ps.nprod = (k >= 2 && n >= 500000) ? 1 : 2;
-        if (const char *g = std::getenv("BILUK_NPROD")) P.ps.nprod = std::atoi(g) == 1 ? 1 : 2;
+        // producer warps (each streams its share of the records into its share
+        // of the ring): four with fill -- smaller records, more copies in
+        // flight (128^3 ILU(2) 3081 vs 3162 us with one, 3478 with two; 100^3 b4
+        // ILU(1) 1609 vs 1686; 128^3 ILU(1) 1478 vs 1511; 64^3 622 vs 626);
+        // two for ILU(0), whose large U' records need the bigger shares (511 vs
+        // 526 us with four, 668 with one)
+        P.ps.nprod = (k >= 1 && bs <= 4) ? 4 : 2;
+        if (const char *g = std::getenv("BILUK_NPROD")) {
+            const int v = std::atoi(g);
+            P.ps.nprod = (v >= 3 && v <= 4 && bs <= 4) ? v : (v == 1 ? 1 : 2);
+        }
         if (const char *g = std::getenv("BILUK_GROUPS")) P.ps.groups = std::atoi(g) == 3 ? 3 : 2;
         if (rc == BILUK_EUNSUPPORTED || (rc == BILUK_OK && !env && per_part > limit)) {
             P.engine = 0;

@@ -705,6 +705,8 @@ static const void *psweep_fn(int groups, int nprod) {
     if (groups == 2)
         return nprod == 1 ? reinterpret_cast<const void *>(psweep_kernel<BS, 2, 1>)
                           : reinterpret_cast<const void *>(psweep_kernel<BS, 2, 2>);
+    if (nprod == 4 && BS <= 4) return reinterpret_cast<const void *>(psweep_kernel<BS, 3, 4>);
+    if (nprod == 3 && BS <= 4) return reinterpret_cast<const void *>(psweep_kernel<BS, 3, 3>);
     return nprod == 1 ? reinterpret_cast<const void *>(psweep_kernel<BS, 3, 1>)
                       : reinterpret_cast<const void *>(psweep_kernel<BS, 3, 2>);
 }

@@ -335,7 +335,7 @@ def test_grid_sweep_declines_other_patterns(b2, monkeypatch):
     assert b2.build_preconditioner(b2.BcsrMatrix(bs, n, n, rp, ci, vals), 0).info["engine"] == 1
 
 
-@pytest.mark.parametrize("groups,nprod", [(3, 1), (2, 2), (2, 1), (3, 2)])
+@pytest.mark.parametrize("groups,nprod", [(3, 1), (2, 2), (2, 1), (3, 2), (3, 3), (3, 4)])
 @pytest.mark.parametrize("case", ["grid16_b3_k0", "grid12_b3_k2", "grid10_b4_k1", "rand300_b3_k1"])
 def test_partitioned_kernel_variants_match_oracle(b2, monkeypatch, groups, nprod, case):
     """Every instantiation of the partitioned sweep (compute groups x producer
